@@ -1,0 +1,173 @@
+/*
+ * lane_allreduce.h — C ABI of the B200-native k-split multi-lane allreduce.
+ *
+ * The operation (PAPER.md = arXiv 2508.13397, cited as P Lnnn):
+ *   MPI_Allreduce(sendbuf, recvbuf, s, MPI_SUM, comm)            P L341-343
+ * computed as the multi-lane algorithm (Alg. 2 "lane_allreduce", P L218-251):
+ *   (1) reduce-scatter among the G GPUs of a node (comm_group)  P L243
+ *   (2) allreduce of slice g among GPU g of every node (comm_lane) P L246
+ *   (3) allgatherv among the G GPUs of the node                 P L248
+ * with the buffer split into k slices ("processes per GPU", l_r, offset
+ * s*l_r, count s/PPG; P L330-349, §3.1.2 P L364-373), each slice reduced by
+ * its own independent group of CTAs.
+ *
+ * Every phase runs in the library's own sm_100a kernel, which loads/stores
+ * peer GPUs' IPC-mapped memory over NVLink 5 / NVSwitch and signals with
+ * .sys-scope release/acquire flags. No NCCL, no CPU fallback.
+ *
+ * Conventions
+ *   - Ranks: p = a*G + g (node a, GPU-in-node g), node-major.
+ *   - Every function returns a lane_status_t (0 = LANE_OK); it never throws
+ *     and never aborts the process. lane_allreduce_last_error() names the
+ *     offending field ("configuration error naming the field").
+ *   - Streams are passed as void* (a cudaStream_t; NULL = legacy default).
+ *   - Device pointers must be device memory of the comm's device, 16-byte
+ *     aligned (LANE_ERR_MISALIGNED otherwise). Any count is accepted.
+ *   - Results are deterministic and identical on every rank: each element is
+ *     reduced once, in the canonical order (ascending GPU index within the
+ *     node, then ascending node), accumulating in fp32 (int32: wrap-around);
+ *     bf16 is rounded to nearest-even once per reducing phase
+ *     (readings R#7-R#9).
+ */
+#ifndef LANE_ALLREDUCE_H
+#define LANE_ALLREDUCE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct lane_comm_s* lane_comm_t;
+
+typedef enum { LANE_INT32 = 0, LANE_FLOAT32 = 1, LANE_BFLOAT16 = 2 } lane_dtype_t;
+
+/* The paper reduces with MPI_SUM only (P L341, L347). */
+typedef enum { LANE_SUM = 0 } lane_op_t;
+
+typedef enum {
+  LANE_OK = 0,
+  LANE_ERR_INVALID_ARG = -1,   /* bad topology/argument; last_error names it   */
+  LANE_ERR_UNSUPPORTED = -2,   /* dtype or op outside the enums                */
+  LANE_ERR_CUDA = -3,          /* a CUDA runtime call or launch failed         */
+  LANE_ERR_NOT_CONNECTED = -4, /* lane_allreduce before lane_allreduce_open_peers
+                                  (resolving an unpublished handle) */
+  LANE_ERR_TIMEOUT = -5,       /* a device-side wait exceeded LANE_TIMEOUT_MS in
+                                  an earlier call; the comm is unusable (finalize) */
+  LANE_ERR_MISALIGNED = -6     /* a buffer pointer is not 16-byte aligned      */
+} lane_status_t;
+
+#define LANE_MAX_RANKS 16         /* N*G; one 8-GPU box uses <= 8                 */
+#define LANE_MAX_PROCS_PER_GPU 16 /* k; the paper's largest PPG is 16 (P L431)    */
+#define LANE_HANDLE_BYTES 256     /* size of one rank's blob from get_handle      */
+
+/* ---------------------------------------------------------------- multi-GPU
+ * One process per GPU (torchrun). Collective: every rank calls init, then
+ * get_handle; the caller all-gathers the P blobs in rank order (the paper
+ * broadcasts IPC handles the same way, P L330) and every rank calls
+ * open_peers. Only then may lane_allreduce be called.
+ */
+
+/* Create a comm for (nodes, gpus_per_node, procs_per_gpu) = (N, G, k).
+ * rank and device are read from $RANK and $LOCAL_RANK (torchrun); requires
+ * N*G == $WORLD_SIZE. Allocates this rank's symmetric scratch and signal
+ * memory on the device (sized by $LANE_ROUND_BYTES, default 1 GiB of message
+ * per round). Errors: INVALID_ARG (any factor < 1, N*G > LANE_MAX_RANKS,
+ * k > LANE_MAX_PROCS_PER_GPU, N*G != WORLD_SIZE, missing env), CUDA. */
+int lane_allreduce_init(int nodes, int gpus_per_node, int procs_per_gpu, lane_comm_t* comm);
+
+/* As lane_allreduce_init with an explicit rank in [0, N*G) and CUDA device. */
+int lane_allreduce_init_rank(int nodes, int gpus_per_node, int procs_per_gpu, int rank,
+                             int device, lane_comm_t* comm);
+
+/* Write this rank's IPC blob (at most LANE_HANDLE_BYTES) into blob;
+ * *blob_bytes receives its size. The caller owns blob. */
+int lane_allreduce_get_handle(lane_comm_t comm, void* blob, size_t* blob_bytes);
+
+/* all_blobs: N*G blobs of blob_bytes each, in rank order (own blob included).
+ * Opens every peer's scratch/signal memory (cudaIpcOpenMemHandle) and checks
+ * that all blobs describe the same (N, G, k) and geometry (INVALID_ARG
+ * otherwise). The mappings are owned by the comm until finalize. */
+int lane_allreduce_open_peers(lane_comm_t comm, const void* all_blobs, size_t blob_bytes);
+
+/* Enqueue the allreduce of count elements on stream; returns immediately.
+ * sendbuf/recvbuf: device pointers owned by the caller, count elements each,
+ * kept alive until the stream passes this point. sendbuf == recvbuf is
+ * in-place; partial overlap is INVALID_ARG. count == 0 is a no-op. Every
+ * rank must call with the same (count, dtype, op) in the same order (MPI
+ * collective semantics, P L341). Messages larger than the round capacity are
+ * processed in several rounds (kernel launches) inside one call. */
+int lane_allreduce(lane_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                   lane_dtype_t dtype, lane_op_t op, void* stream);
+
+/* End-to-end variant on HOST buffers: copies host_send to a library-owned
+ * device staging buffer, runs lane_allreduce, copies the result to host_recv,
+ * all on stream (pinned host memory gives async copies). The caller
+ * synchronizes the stream before reading host_recv. */
+int lane_allreduce_host(lane_comm_t comm, const void* host_send, void* host_recv, size_t count,
+                        lane_dtype_t dtype, lane_op_t op, void* stream);
+
+/* ------------------------------------------------------------- emulated mode
+ * All P = N*G ranks on ONE device: every rank's scratch lives in this
+ * device's HBM and one cooperative launch runs every rank's CTAs, so the same
+ * kernels (and the same cross-rank flag protocol) run without NVLink. Used
+ * for single-GPU parity and for the N=1 benchmark. */
+int lane_allreduce_init_emulated(int nodes, int gpus_per_node, int procs_per_gpu, int device,
+                                 lane_comm_t* comm);
+
+/* sendbufs/recvbufs: host arrays of N*G device pointers (rank order). */
+int lane_allreduce_emulated(lane_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
+                            size_t count, lane_dtype_t dtype, lane_op_t op, void* stream);
+
+/* Emulated end-to-end variant: host arrays of N*G HOST buffer pointers. */
+int lane_allreduce_emulated_host(lane_comm_t comm, const void* const* host_sends,
+                                 void* const* host_recvs, size_t count, lane_dtype_t dtype,
+                                 lane_op_t op, void* stream);
+
+/* ----------------------------------------------------------------- common */
+
+/* Release scratch, IPC mappings and staging. Collective in multi-GPU mode:
+ * call only after every rank's last lane_allreduce has completed. */
+int lane_allreduce_finalize(lane_comm_t comm);
+
+/* Human-readable reason for the last error on comm (never NULL). */
+const char* lane_allreduce_last_error(lane_comm_t comm);
+
+/* Poll the device-side error word (set by the wait watchdog). Returns
+ * LANE_OK or LANE_ERR_TIMEOUT. Does not synchronize. */
+int lane_allreduce_check(lane_comm_t comm);
+
+/* The execution plan lane_allreduce uses for (count, dtype): chunk size and
+ * round size in 16-byte granules, CTAs per CTA group, kernel launches
+ * (rounds) per call. Any out-pointer may be NULL. */
+int lane_allreduce_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype,
+                        int64_t* chunk_granules, int64_t* round_granules, int* ctas_per_group,
+                        int* launches);
+
+/* -------------------------------------------------- host-only introspection
+ * No GPU needed; used by the CPU test-suite to compare the library's own
+ * topology and partition with the oracle's. */
+
+/* Topology of rank p: node, gpu, comm_group ranks (G
+ * entries) and comm_lane ranks (N entries); any out-pointer may be NULL. */
+int lane_topology_query(int nodes, int gpus_per_node, int rank, int* node, int* gpu,
+                        int* group_ranks, int* lane_ranks);
+
+/* Enumerate the ownership units of a message exactly as the kernels
+ * partition it: for each unit, 9 int64 values
+ * {round, l, c, g, a, part_start, part_end, start, end} (element indices).
+ * chunk_granules / round_granules <= 0 mean "one piece". Writes at most
+ * max_units units to units_out (may be NULL) and the total in *n_units. */
+int lane_partition_query(uint64_t count, int itemsize, int nodes, int gpus_per_node,
+                         int procs_per_gpu, int64_t chunk_granules, int64_t round_granules,
+                         int64_t* units_out, uint64_t max_units, uint64_t* n_units);
+
+/* Library version string. */
+const char* lane_allreduce_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* LANE_ALLREDUCE_H */

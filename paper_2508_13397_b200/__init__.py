@@ -1,0 +1,222 @@
+"""B200-native k-split multi-lane allreduce (arXiv 2508.13397).
+
+Thin Python binding over the C ABI in ``include/lane_allreduce.h``
+(liblane_allreduce.so, sm_100a). PyTorch is used for device memory, streams
+and the one-time IPC handle exchange (``torch.distributed``); every step of
+the allreduce runs in the library's CUDA kernels.
+
+    comm = LaneComm(nodes=2, gpus_per_node=4, procs_per_gpu=1)   # under torchrun
+    comm.allreduce(out, inp)                                      # out = sum over ranks
+
+    emu = LaneEmulator(2, 4, 1)          # all 8 ranks on one GPU (same kernels)
+    emu.allreduce(outs, inps)
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._lib import DTYPE, HANDLE_BYTES, LaneError
+
+__all__ = ["LaneComm", "LaneEmulator", "LaneError", "topology", "partition_units", "version"]
+
+
+def _torch():
+    import torch
+    return torch
+
+
+def _dtype_code(t) -> int:
+    torch = _torch()
+    m = {torch.int32: DTYPE["int32"], torch.float32: DTYPE["float32"], torch.bfloat16: DTYPE["bfloat16"]}
+    if t.dtype not in m:
+        raise LaneError(-2, f"dtype: {t.dtype} is not supported (int32, float32, bfloat16)")
+    return m[t.dtype]
+
+
+def _check_dev_tensor(t, device_index: int, what: str):
+    if not t.is_cuda or t.device.index != device_index:
+        raise LaneError(-1, f"{what}: must be a CUDA tensor on device {device_index}")
+    if not t.is_contiguous():
+        raise LaneError(-1, f"{what}: must be contiguous")
+
+
+def _stream_handle(stream) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def version() -> str:
+    return _lib.load().lane_allreduce_version().decode()
+
+
+def topology(nodes: int, gpus_per_node: int, rank: int):
+    """(node, gpu, comm_group ranks, comm_lane ranks) of ``rank`` — host only."""
+    lib = _lib.load()
+    node, gpu = ctypes.c_int(), ctypes.c_int()
+    grp = (ctypes.c_int * max(gpus_per_node, 1))()
+    lane = (ctypes.c_int * max(nodes, 1))()
+    _lib.check(lib.lane_topology_query(nodes, gpus_per_node, rank, ctypes.byref(node), ctypes.byref(gpu),
+                                       grp, lane))
+    return node.value, gpu.value, list(grp)[:gpus_per_node], list(lane)[:nodes]
+
+
+def partition_units(count: int, itemsize: int, nodes: int, gpus_per_node: int, procs_per_gpu: int,
+                    chunk_granules: int = 0, round_granules: int = 0):
+    """The library's ownership units (host only): list of 9-tuples
+    (round, l, c, g, a, part_start, part_end, start, end)."""
+    lib = _lib.load()
+    n = ctypes.c_uint64()
+    _lib.check(lib.lane_partition_query(count, itemsize, nodes, gpus_per_node, procs_per_gpu,
+                                        chunk_granules, round_granules, None, 0, ctypes.byref(n)))
+    buf = (ctypes.c_int64 * (9 * max(n.value, 1)))()
+    _lib.check(lib.lane_partition_query(count, itemsize, nodes, gpus_per_node, procs_per_gpu,
+                                        chunk_granules, round_granules, buf, n.value, ctypes.byref(n)))
+    flat = list(buf)
+    return [tuple(flat[9 * i:9 * i + 9]) for i in range(n.value)]
+
+
+class _CommBase:
+    _comm = None
+
+    def plan(self, count: int, dtype: str = "float32") -> dict:
+        lib = _lib.load()
+        cg, rg = ctypes.c_int64(), ctypes.c_int64()
+        C, launches = ctypes.c_int(), ctypes.c_int()
+        _lib.check(lib.lane_allreduce_plan(self._comm, count, DTYPE[dtype], ctypes.byref(cg), ctypes.byref(rg),
+                                           ctypes.byref(C), ctypes.byref(launches)), self._comm)
+        return {"chunk_granules": cg.value, "round_granules": rg.value, "ctas_per_group": C.value,
+                "launches": launches.value}
+
+    def check(self) -> None:
+        _lib.check(_lib.load().lane_allreduce_check(self._comm), self._comm)
+
+    def close(self) -> None:
+        if self._comm is not None:
+            _lib.load().lane_allreduce_finalize(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class LaneComm(_CommBase):
+    """One rank of a multi-GPU lane allreduce (one process per GPU).
+
+    ``nodes * gpus_per_node`` must equal the world size; rank ``p`` is
+    virtual node ``p // gpus_per_node``, GPU ``p % gpus_per_node``. The IPC
+    handles are all-gathered through ``torch.distributed`` (``group``, default
+    world) once, at construction — the only host-side collective."""
+
+    def __init__(self, nodes: int, gpus_per_node: int, procs_per_gpu: int = 1, *, rank=None,
+                 device=None, group=None):
+        torch = _torch()
+        import torch.distributed as dist
+        lib = _lib.load()
+        if rank is None:
+            rank = dist.get_rank(group) if dist.is_initialized() else 0
+        if device is None:
+            device = torch.cuda.current_device()
+        self.nodes, self.gpus_per_node, self.procs_per_gpu = nodes, gpus_per_node, procs_per_gpu
+        self.rank, self.device = rank, device
+        h = ctypes.c_void_p()
+        code = lib.lane_allreduce_init_rank(nodes, gpus_per_node, procs_per_gpu, rank, device, ctypes.byref(h))
+        _lib.check(code, None)
+        self._comm = h
+        blob = ctypes.create_string_buffer(HANDLE_BYTES)
+        size = ctypes.c_size_t()
+        _lib.check(lib.lane_allreduce_get_handle(self._comm, blob, ctypes.byref(size)), self._comm)
+        blobs = exchange_blobs(bytes(blob.raw[:size.value]), group)
+        if len(blobs) != nodes * gpus_per_node:
+            raise LaneError(-1, f"world size {len(blobs)} != nodes*gpus_per_node {nodes * gpus_per_node}")
+        allb = b"".join(blobs)
+        _lib.check(lib.lane_allreduce_open_peers(self._comm, allb, size.value), self._comm)
+
+    def allreduce(self, out, inp, op: str = "sum", stream=None):
+        """out[i] = sum over ranks of inp[i]; enqueued on ``stream`` (default:
+        current). ``out is inp`` (same storage) is in-place."""
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        _check_dev_tensor(inp, self.device, "inp")
+        _check_dev_tensor(out, self.device, "out")
+        if out.numel() != inp.numel() or out.dtype != inp.dtype:
+            raise LaneError(-1, "out: must match inp in numel and dtype")
+        code = _lib.load().lane_allreduce(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
+                                          _dtype_code(inp), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return out
+
+    def allreduce_host(self, out_host, inp_host, stream=None):
+        """End-to-end allreduce of HOST tensors (H2D, kernels, D2H on one
+        stream). Synchronizes the stream before returning."""
+        torch = _torch()
+        code = _lib.load().lane_allreduce_host(self._comm, inp_host.data_ptr(), out_host.data_ptr(),
+                                               inp_host.numel(), _dtype_code(inp_host), 0,
+                                               _stream_handle(stream))
+        _lib.check(code, self._comm)
+        (stream or torch.cuda.current_stream()).synchronize()
+        return out_host
+
+
+def exchange_blobs(blob: bytes, group=None) -> list[bytes]:
+    """All-gather one opaque blob per rank, in rank order (IPC handle
+    broadcast, P L330). Uses torch.distributed; works on gloo and nccl."""
+    import torch.distributed as dist
+    if not dist.is_initialized():
+        return [blob]
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, blob, group=group)
+    return out
+
+
+class LaneEmulator(_CommBase):
+    """All ``nodes * gpus_per_node`` ranks on ONE GPU: the same kernels and the
+    same cross-rank flag protocol, run as one cooperative launch."""
+
+    def __init__(self, nodes: int, gpus_per_node: int, procs_per_gpu: int = 1, device=None):
+        torch = _torch()
+        lib = _lib.load()
+        if device is None:
+            device = torch.cuda.current_device()
+        self.nodes, self.gpus_per_node, self.procs_per_gpu = nodes, gpus_per_node, procs_per_gpu
+        self.P = nodes * gpus_per_node
+        self.device = device
+        h = ctypes.c_void_p()
+        _lib.check(lib.lane_allreduce_init_emulated(nodes, gpus_per_node, procs_per_gpu, device, ctypes.byref(h)),
+                   None)
+        self._comm = h
+
+    def _ptrs(self, ts, what, dev=True):
+        if len(ts) != self.P:
+            raise LaneError(-1, f"{what}: need {self.P} tensors, got {len(ts)}")
+        for i, t in enumerate(ts):
+            if dev:
+                _check_dev_tensor(t, self.device, f"{what}[{i}]")
+            elif t.is_cuda or not t.is_contiguous():
+                raise LaneError(-1, f"{what}[{i}]: must be a contiguous host tensor")
+        return (ctypes.c_void_p * self.P)(*[t.data_ptr() for t in ts])
+
+    def allreduce(self, outs, inps, op: str = "sum", stream=None):
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        n = inps[0].numel()
+        if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
+            raise LaneError(-1, "all tensors must have the same numel and dtype")
+        code = _lib.load().lane_allreduce_emulated(self._comm, self._ptrs(inps, "inps"), self._ptrs(outs, "outs"),
+                                                   n, _dtype_code(inps[0]), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return outs
+
+    def allreduce_host(self, outs_host, inps_host, stream=None):
+        torch = _torch()
+        n = inps_host[0].numel()
+        code = _lib.load().lane_allreduce_emulated_host(
+            self._comm, self._ptrs(inps_host, "inps", dev=False), self._ptrs(outs_host, "outs", dev=False), n,
+            _dtype_code(inps_host[0]), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        (stream or torch.cuda.current_stream()).synchronize()
+        return outs_host

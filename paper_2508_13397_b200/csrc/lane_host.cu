@@ -1,0 +1,668 @@
+// lane_host.cu — host runtime and C ABI of the multi-lane allreduce.
+//
+// Components: topology / lane map (N1), granule partition +
+// chunk plan (N2), IPC buffer registry for the symmetric scratch and signal
+// memory (N3), the multi-CTA-group scheduler / launcher (N8) and the C ABI
+// (N9) declared in include/lane_allreduce.h.
+//
+// The paper's multi-PPG setup (P L330: the leader allocates, publishes an IPC
+// handle, the others open it) becomes: every rank allocates ONE symmetric
+// scratch allocation, publishes its cudaIpcMemHandle through the caller's
+// all-gather, and opens every peer's. There is one process per GPU; the
+// paper's k processes per GPU become k CTA groups inside the kernel.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include <unistd.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/lane_allreduce.h"
+#include "lane_kernels.cuh"
+#include "lane_plan.h"
+
+using lane::LaneParams;
+using lane::RankMem;
+using lane::Span;
+
+namespace {
+
+constexpr uint32_t kMagic = 0x4C414E45u;  // "LANE"
+constexpr int kVersion = 1;
+
+struct Blob {
+  uint32_t magic;
+  int32_t version;
+  int32_t N, G, k, rank, device, pid;
+  uint64_t s1_bytes, s2_bytes, r_bytes, flag_bytes, total_bytes;
+  int64_t round_cap, chunk_cap;
+  cudaIpcMemHandle_t handle;
+};
+static_assert(sizeof(Blob) <= LANE_HANDLE_BYTES, "blob too large");
+
+int64_t env_i64(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  char* end = nullptr;
+  long long x = strtoll(v, &end, 10);
+  if (end == v) return dflt;
+  return (int64_t)x;
+}
+
+}  // namespace
+
+struct lane_comm_s {
+  int N = 0, G = 0, P = 0, k = 0, rank = 0, device = 0;
+  bool emulated = false;
+  bool connected = false;
+  int threads = 512;
+  int ctas_per_group = 0;  // 0 = choose per call
+  int max_coresident = 0;  // CTAs of the kernel that fit on the device at once
+  int sm_count = 0;
+  int64_t round_cap = 0;   // granules of message per round (kernel launch)
+  int64_t cg_max = 0, cg_min = 0;
+  int64_t chunk_cap = 0;   // max chunks per round (flag capacity per flag type)
+  uint64_t s1_bytes = 0, s2_bytes = 0, r_bytes = 0, flag_bytes = 0, total_bytes = 0;
+  std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
+  std::vector<void*> opened; // IPC-opened peer allocations
+  RankMem rk[LANE_MAX_RANKS];
+  cudaIpcMemHandle_t handle;
+  uint32_t epoch = 0;
+  uint32_t* err_host = nullptr;  // mapped pinned word
+  uint32_t* err_dev = nullptr;
+  uint32_t* abort_dev = nullptr;
+  uint64_t timeout_ns = 0;
+  std::vector<char*> stage;  // device staging for the host-buffer API
+  uint64_t stage_bytes = 0;
+  std::string last_error;
+};
+
+namespace {
+
+int fail(lane_comm_t c, int code, const std::string& msg) {
+  if (c) c->last_error = msg;
+  return code;
+}
+
+int cuda_fail(lane_comm_t c, cudaError_t e, const char* what) {
+  std::string m = std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")";
+  return fail(c, LANE_ERR_CUDA, m);
+}
+
+#define LANE_CUDA(c, call)                                   \
+  do {                                                       \
+    cudaError_t e_ = (call);                                 \
+    if (e_ != cudaSuccess) return cuda_fail((c), e_, #call); \
+  } while (0)
+
+int validate_topology(int N, int G, int k, std::string* why) {
+  if (N < 1) return *why = "nodes must be >= 1", LANE_ERR_INVALID_ARG;
+  if (G < 1) return *why = "gpus_per_node must be >= 1", LANE_ERR_INVALID_ARG;
+  if (k < 1) return *why = "procs_per_gpu must be >= 1", LANE_ERR_INVALID_ARG;
+  if ((int64_t)N * G > LANE_MAX_RANKS)
+    return *why = "nodes*gpus_per_node exceeds LANE_MAX_RANKS", LANE_ERR_INVALID_ARG;
+  if (k > LANE_MAX_PROCS_PER_GPU)
+    return *why = "procs_per_gpu exceeds LANE_MAX_PROCS_PER_GPU", LANE_ERR_INVALID_ARG;
+  return LANE_OK;
+}
+
+int itemsize_of(int dtype) { return dtype == LANE_BFLOAT16 ? 2 : 4; }
+
+// Geometry of one rank's scratch for a comm (sizes in bytes). Every call's
+// plan fits by construction: with round_len <= round_cap, CG in
+// [cg_min, cg_max] and at most round_cap/CG + k chunks, a slot region needs
+// chunks * ceil(CG/G) <= round_cap/G + round_cap/cg_min + k*(cg_max/G + 1).
+void size_scratch(lane_comm_t c) {
+  const int64_t RC = c->round_cap, G = c->G, N = c->N, k = c->k;
+  c->chunk_cap = RC / c->cg_min + k + 1;
+  const int64_t slot_g = RC / G + RC / c->cg_min + k * (c->cg_max / G + 1) + 16;
+  const int64_t slot_u = RC / (G * N) + RC / c->cg_min + k * (c->cg_max / (G * N) + 1) + 16;
+  c->s1_bytes = (uint64_t)((G - 1) * slot_g) * 16;
+  c->s2_bytes = (uint64_t)(N * slot_u) * 16;
+  c->r_bytes = (uint64_t)slot_g * 16;
+  c->flag_bytes = (uint64_t)((2 * G + 2 * N) * c->chunk_cap) * 4;
+  auto al = [](uint64_t x) { return (x + 4095) & ~(uint64_t)4095; };
+  c->s1_bytes = al(c->s1_bytes);
+  c->s2_bytes = al(c->s2_bytes);
+  c->r_bytes = al(c->r_bytes);
+  c->flag_bytes = al(c->flag_bytes);
+  c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes;
+}
+
+void carve(lane_comm_t c, char* base, RankMem* m) {
+  m->s1 = base;
+  m->s2 = base + c->s1_bytes;
+  m->r = base + c->s1_bytes + c->s2_bytes;
+  m->flags = reinterpret_cast<uint32_t*>(base + c->s1_bytes + c->s2_bytes + c->r_bytes);
+  m->send = nullptr;
+  m->recv = nullptr;
+}
+
+template <int DT>
+int occupancy_of(int threads) {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::lane_allreduce_kernel<DT>, threads, 0);
+  return nb;
+}
+
+thread_local std::string g_init_error;  // errors of init calls that return no comm
+
+int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, bool emulated) {
+  c->N = N;
+  c->G = G;
+  c->P = N * G;
+  c->k = k;
+  c->rank = rank;
+  c->device = device;
+  c->emulated = emulated;
+  c->threads = (int)env_i64("LANE_THREADS", 512);
+  if (c->threads < 64 || c->threads > 512 || c->threads % 32)
+    return fail(c, LANE_ERR_INVALID_ARG, "LANE_THREADS must be a multiple of 32 in [64, 512]");
+  c->ctas_per_group = (int)env_i64("LANE_CTAS_PER_GROUP", 0);
+  c->round_cap = env_i64("LANE_ROUND_BYTES", (int64_t)1 << 30) / 16;
+  c->cg_max = env_i64("LANE_CHUNK_BYTES", 256 << 10) / 16;
+  c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 16 << 10) / 16;
+  if (c->round_cap < 1024) return fail(c, LANE_ERR_INVALID_ARG, "LANE_ROUND_BYTES must be >= 16 KiB");
+  if (c->cg_min < 16) c->cg_min = 16;
+  if (c->cg_max < c->cg_min) c->cg_max = c->cg_min;
+  c->timeout_ns = (uint64_t)env_i64("LANE_TIMEOUT_MS", 20000) * 1000000ull;
+  size_scratch(c);
+
+  LANE_CUDA(c, cudaSetDevice(device));
+  LANE_CUDA(c, cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+  int occ = occupancy_of<0>(c->threads);
+  int o1 = occupancy_of<1>(c->threads), o2 = occupancy_of<2>(c->threads);
+  occ = occ < o1 ? occ : o1;
+  occ = occ < o2 ? occ : o2;
+  if (occ < 1) occ = 1;
+  c->max_coresident = occ * c->sm_count;
+
+  const int nalloc = emulated ? c->P : 1;
+  for (int i = 0; i < nalloc; ++i) {
+    char* p = nullptr;
+    LANE_CUDA(c, cudaMalloc(&p, c->total_bytes));
+    c->own.push_back(p);
+    // flags must read 0 before any peer can write an epoch >= 1
+    LANE_CUDA(c, cudaMemset(p + c->s1_bytes + c->s2_bytes + c->r_bytes, 0, c->flag_bytes));
+  }
+  LANE_CUDA(c, cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
+  memset(c->err_host, 0, 64);
+  LANE_CUDA(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
+  LANE_CUDA(c, cudaMalloc(&c->abort_dev, 64));
+  LANE_CUDA(c, cudaMemset(c->abort_dev, 0, 64));
+  LANE_CUDA(c, cudaDeviceSynchronize());
+  if (emulated) {
+    for (int p = 0; p < c->P; ++p) carve(c, c->own[p], &c->rk[p]);
+    c->connected = true;
+  } else {
+    carve(c, c->own[0], &c->rk[c->rank]);
+    LANE_CUDA(c, cudaIpcGetMemHandle(&c->handle, c->own[0]));
+  }
+  return LANE_OK;
+}
+
+void release(lane_comm_t c);
+
+int common_init(int N, int G, int k, int rank, int device, bool emulated, lane_comm_t* out) {
+  *out = nullptr;
+  std::string why;
+  int st = validate_topology(N, G, k, &why);
+  if (st != LANE_OK) {
+    g_init_error = why;
+    return st;
+  }
+  lane_comm_t c = new lane_comm_s();
+  st = common_init_impl(c, N, G, k, rank, device, emulated);
+  if (st != LANE_OK) {
+    g_init_error = c->last_error;
+    release(c);
+    return st;
+  }
+  *out = c;
+  return LANE_OK;
+}
+
+bool overlaps_partially(const void* s, const void* r, uint64_t bytes) {
+  uintptr_t a = (uintptr_t)s, b = (uintptr_t)r;
+  if (a == b) return false;
+  return a < b + bytes && b < a + bytes;
+}
+
+struct Plan {
+  int64_t ng, cg, round_len0;
+  int rounds, C, tail_elems, q;
+};
+
+int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
+  const int isz = itemsize_of(dtype);
+  pl->q = 16 / isz;
+  pl->ng = (int64_t)((count + pl->q - 1) / pl->q);
+  pl->tail_elems = (int)(count - (uint64_t)(pl->ng - 1) * pl->q);
+  pl->round_len0 = pl->ng < c->round_cap ? pl->ng : c->round_cap;
+  pl->rounds = (int)((pl->ng + c->round_cap - 1) / c->round_cap);
+  // CTAs per CTA group: fill the device with all ranks' groups (emulated) or
+  // default to 64 CTAs per GPU across the k groups (multi-GPU); env override.
+  int ranks_here = c->emulated ? c->P : 1;
+  int C = c->ctas_per_group;
+  if (C <= 0) {
+    int budget = c->emulated ? c->max_coresident : (int)env_i64("LANE_CTAS_TOTAL", 64);
+    C = budget / (ranks_here * c->k);
+    if (C > 64) C = 64;
+  }
+  if (C < 1) C = 1;
+  if ((int64_t)C * c->k * ranks_here > c->max_coresident)
+    return fail(c, LANE_ERR_INVALID_ARG,
+                "ctas_per_group*procs_per_gpu exceeds the device's co-resident CTA capacity");
+  pl->C = C;
+  // chunk size: give every CTA of a group at least one chunk, within bounds
+  int64_t slice0 = (pl->round_len0 + c->k - 1) / c->k;
+  int64_t cg = (slice0 + C - 1) / C;
+  if (cg > c->cg_max) cg = c->cg_max;
+  if (cg < c->cg_min) cg = c->cg_min;
+  pl->cg = cg;
+  return LANE_OK;
+}
+
+LaneParams base_params(lane_comm_t c, const Plan& pl) {
+  LaneParams p;
+  memset(&p, 0, sizeof(p));
+  for (int r = 0; r < c->P; ++r) p.rk[r] = c->rk[r];
+  p.N = c->N;
+  p.G = c->G;
+  p.P = c->P;
+  p.k = c->k;
+  p.C = pl.C;
+  p.q = pl.q;
+  p.tail_elems = pl.tail_elems;
+  p.ng = pl.ng;
+  p.cg = pl.cg;
+  p.sg = lane::ceil_div(pl.cg, c->G);
+  p.su = lane::ceil_div(p.sg, c->N);
+  p.timeout_ns = c->timeout_ns;
+  p.err = c->err_dev;
+  p.abort_flag = c->abort_dev;
+  return p;
+}
+
+int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
+  const int nlocal = p.nlocal;
+  for (int r = 0; r < pl.rounds; ++r) {
+    p.round_g0 = (int64_t)r * c->round_cap;
+    int64_t rest = pl.ng - p.round_g0;
+    p.round_len = rest < c->round_cap ? rest : c->round_cap;
+    p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
+    if (p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
+    p.epoch = ++c->epoch;
+    dim3 grid((unsigned)(nlocal * c->k * p.C)), block((unsigned)c->threads);
+    cudaError_t e;
+    void* args[] = {&p};
+    const void* fn = dtype == LANE_INT32     ? (const void*)lane::lane_allreduce_kernel<0>
+                     : dtype == LANE_FLOAT32 ? (const void*)lane::lane_allreduce_kernel<1>
+                                             : (const void*)lane::lane_allreduce_kernel<2>;
+    if (c->emulated)
+      e = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s);
+    else
+      e = cudaLaunchKernel(fn, grid, block, args, 0, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, "lane_allreduce_kernel launch");
+  }
+  return LANE_OK;
+}
+
+int check_call(lane_comm_t c, uint64_t count, int dtype, int op) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
+    return fail(c, LANE_ERR_UNSUPPORTED, "dtype: unsupported lane_dtype_t");
+  if (op != LANE_SUM) return fail(c, LANE_ERR_UNSUPPORTED, "op: only LANE_SUM (MPI_SUM, P L341)");
+  if (!c->connected)
+    return fail(c, LANE_ERR_NOT_CONNECTED, "comm: lane_allreduce_open_peers has not completed");
+  if (c->err_host && *(volatile uint32_t*)c->err_host)
+    return fail(c, LANE_ERR_TIMEOUT, "comm: a device-side wait timed out in an earlier call");
+  (void)count;
+  return LANE_OK;
+}
+
+int check_buffers(lane_comm_t c, const void* s, const void* r, uint64_t bytes, const char* which) {
+  if (!s || !r) return fail(c, LANE_ERR_INVALID_ARG, std::string(which) + ": null buffer");
+  if (((uintptr_t)s | (uintptr_t)r) & 15)
+    return fail(c, LANE_ERR_MISALIGNED, std::string(which) + ": buffers must be 16-byte aligned");
+  if (overlaps_partially(s, r, bytes))
+    return fail(c, LANE_ERR_INVALID_ARG, std::string(which) + ": sendbuf and recvbuf partially overlap");
+  return LANE_OK;
+}
+
+int copy_p1(lane_comm_t c, const void* s, void* r, const Plan& pl, cudaStream_t st) {
+  if (s == r) return LANE_OK;
+  const int tail_bytes = pl.tail_elems < pl.q ? pl.tail_elems * (16 / pl.q) : 0;
+  int64_t blocks = (pl.ng + 511) / 512;
+  if (blocks > (int64_t)c->sm_count * 4) blocks = (int64_t)c->sm_count * 4;
+  lane::lane_copy_kernel<<<(unsigned)blocks, 512, 0, st>>>(
+      reinterpret_cast<const uint4*>(s), reinterpret_cast<uint4*>(r), pl.ng, tail_bytes);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return cuda_fail(c, e, "lane_copy_kernel launch");
+  return LANE_OK;
+}
+
+int ensure_stage(lane_comm_t c, uint64_t bytes) {
+  const int nbuf = 2 * (c->emulated ? c->P : 1);
+  if (c->stage_bytes >= bytes && (int)c->stage.size() == nbuf) return LANE_OK;
+  for (char* p : c->stage) cudaFree(p);
+  c->stage.clear();
+  c->stage_bytes = 0;
+  for (int i = 0; i < nbuf; ++i) {
+    char* p = nullptr;
+    LANE_CUDA(c, cudaMalloc(&p, bytes ? bytes : 16));
+    c->stage.push_back(p);
+  }
+  c->stage_bytes = bytes;
+  return LANE_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* lane_allreduce_version(void) { return "lane_allreduce 0.1 (sm_100a)"; }
+
+int lane_allreduce_init_rank(int nodes, int gpus_per_node, int procs_per_gpu, int rank, int device,
+                             lane_comm_t* comm) {
+  if (!comm) return LANE_ERR_INVALID_ARG;
+  *comm = nullptr;
+  if (rank < 0 || (int64_t)rank >= (int64_t)nodes * gpus_per_node) {
+    int st = validate_topology(nodes, gpus_per_node, procs_per_gpu, &g_init_error);
+    if (st == LANE_OK) g_init_error = "rank: must be in [0, nodes*gpus_per_node)";
+    return LANE_ERR_INVALID_ARG;
+  }
+  return common_init(nodes, gpus_per_node, procs_per_gpu, rank, device, false, comm);
+}
+
+int lane_allreduce_init(int nodes, int gpus_per_node, int procs_per_gpu, lane_comm_t* comm) {
+  if (!comm) return LANE_ERR_INVALID_ARG;
+  *comm = nullptr;
+  const char* r = getenv("RANK");
+  const char* lr = getenv("LOCAL_RANK");
+  const char* ws = getenv("WORLD_SIZE");
+  if (!r || !ws) {
+    g_init_error = "RANK/WORLD_SIZE: not set (use lane_allreduce_init_rank)";
+    return LANE_ERR_INVALID_ARG;
+  }
+  int rank = atoi(r), world = atoi(ws), local = lr ? atoi(lr) : rank;
+  if ((int64_t)nodes * gpus_per_node != world) {
+    g_init_error = "nodes*gpus_per_node: must equal WORLD_SIZE";
+    return LANE_ERR_INVALID_ARG;
+  }
+  return lane_allreduce_init_rank(nodes, gpus_per_node, procs_per_gpu, rank, local, comm);
+}
+
+int lane_allreduce_init_emulated(int nodes, int gpus_per_node, int procs_per_gpu, int device,
+                                 lane_comm_t* comm) {
+  if (!comm) return LANE_ERR_INVALID_ARG;
+  *comm = nullptr;
+  return common_init(nodes, gpus_per_node, procs_per_gpu, 0, device, true, comm);
+}
+
+int lane_allreduce_get_handle(lane_comm_t c, void* blob, size_t* blob_bytes) {
+  if (!c || !blob || !blob_bytes) return fail(c, LANE_ERR_INVALID_ARG, "get_handle: null argument");
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "get_handle: emulated comm has no peers");
+  Blob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagic;
+  b.version = kVersion;
+  b.N = c->N;
+  b.G = c->G;
+  b.k = c->k;
+  b.rank = c->rank;
+  b.device = c->device;
+  b.pid = (int32_t)getpid();
+  b.s1_bytes = c->s1_bytes;
+  b.s2_bytes = c->s2_bytes;
+  b.r_bytes = c->r_bytes;
+  b.flag_bytes = c->flag_bytes;
+  b.total_bytes = c->total_bytes;
+  b.round_cap = c->round_cap;
+  b.chunk_cap = c->chunk_cap;
+  b.handle = c->handle;
+  memcpy(blob, &b, sizeof(b));
+  *blob_bytes = sizeof(b);
+  return LANE_OK;
+}
+
+int lane_allreduce_open_peers(lane_comm_t c, const void* all_blobs, size_t blob_bytes) {
+  if (!c || !all_blobs) return fail(c, LANE_ERR_INVALID_ARG, "open_peers: null argument");
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "open_peers: emulated comm has no peers");
+  if (c->connected) return fail(c, LANE_ERR_INVALID_ARG, "open_peers: already connected");
+  if (blob_bytes < sizeof(Blob)) return fail(c, LANE_ERR_INVALID_ARG, "blob_bytes: too small");
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  const char* base = static_cast<const char*>(all_blobs);
+  for (int p = 0; p < c->P; ++p) {
+    Blob b;
+    memcpy(&b, base + (size_t)p * blob_bytes, sizeof(b));
+    if (b.magic != kMagic || b.version != kVersion)
+      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs[" + std::to_string(p) + "]: not a lane blob");
+    if (b.rank != p) return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: not in rank order");
+    if (b.N != c->N || b.G != c->G || b.k != c->k)
+      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: ranks disagree on (nodes, gpus_per_node, procs_per_gpu)");
+    if (b.total_bytes != c->total_bytes || b.round_cap != c->round_cap || b.chunk_cap != c->chunk_cap)
+      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: ranks disagree on scratch geometry (LANE_* env)");
+    if (p == c->rank) continue;
+    void* ptr = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcOpenMemHandle");
+    c->opened.push_back(ptr);
+    carve(c, static_cast<char*>(ptr), &c->rk[p]);
+  }
+  c->connected = true;
+  return LANE_OK;
+}
+
+int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t count,
+                   lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce: use lane_allreduce_emulated");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  st = check_buffers(c, sendbuf, recvbuf, bytes, "lane_allreduce");
+  if (st != LANE_OK) return st;
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = c->rank;
+  p.nlocal = 1;
+  p.rk[c->rank].send = static_cast<const char*>(sendbuf);
+  p.rk[c->rank].recv = static_cast<char*>(recvbuf);
+  return launch_rounds(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* const* recvbufs,
+                            size_t count, lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (!c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_emulated: comm is not emulated");
+  if (!sendbufs || !recvbufs) return fail(c, LANE_ERR_INVALID_ARG, "sendbufs/recvbufs: null");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  for (int r = 0; r < c->P; ++r) {
+    st = check_buffers(c, sendbufs[r], recvbufs[r], bytes,
+                       ("rank " + std::to_string(r)).c_str());
+    if (st != LANE_OK) return st;
+  }
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = 0;
+  p.nlocal = c->P;
+  for (int r = 0; r < c->P; ++r) {
+    p.rk[r].send = static_cast<const char*>(sendbufs[r]);
+    p.rk[r].recv = static_cast<char*>(recvbufs[r]);
+  }
+  return launch_rounds(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_host(lane_comm_t c, const void* host_send, void* host_recv, size_t count,
+                        lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_host: use lane_allreduce_emulated_host");
+  if (count == 0) return LANE_OK;
+  if (!host_send || !host_recv) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  st = ensure_stage(c, bytes);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  LANE_CUDA(c, cudaMemcpyAsync(c->stage[0], host_send, bytes, cudaMemcpyHostToDevice, s));
+  st = lane_allreduce(c, c->stage[0], c->stage[1], count, dtype, op, stream);
+  if (st != LANE_OK) return st;
+  LANE_CUDA(c, cudaMemcpyAsync(host_recv, c->stage[1], bytes, cudaMemcpyDeviceToHost, s));
+  return LANE_OK;
+}
+
+int lane_allreduce_emulated_host(lane_comm_t c, const void* const* host_sends,
+                                 void* const* host_recvs, size_t count, lane_dtype_t dtype,
+                                 lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (!c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_emulated_host: comm is not emulated");
+  if (count == 0) return LANE_OK;
+  if (!host_sends || !host_recvs) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  st = ensure_stage(c, bytes);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  std::vector<const void*> sends(c->P);
+  std::vector<void*> recvs(c->P);
+  for (int r = 0; r < c->P; ++r) {
+    if (!host_sends[r] || !host_recvs[r]) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+    LANE_CUDA(c, cudaMemcpyAsync(c->stage[2 * r], host_sends[r], bytes, cudaMemcpyHostToDevice, s));
+    sends[r] = c->stage[2 * r];
+    recvs[r] = c->stage[2 * r + 1];
+  }
+  st = lane_allreduce_emulated(c, sends.data(), recvs.data(), count, dtype, op, stream);
+  if (st != LANE_OK) return st;
+  for (int r = 0; r < c->P; ++r)
+    LANE_CUDA(c, cudaMemcpyAsync(host_recvs[r], c->stage[2 * r + 1], bytes, cudaMemcpyDeviceToHost, s));
+  return LANE_OK;
+}
+
+int lane_allreduce_finalize(lane_comm_t c) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  release(c);
+  return LANE_OK;
+}
+
+}  // extern "C"
+
+namespace {
+void release(lane_comm_t c) {
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (char* p : c->own) cudaFree(p);
+  for (char* p : c->stage) cudaFree(p);
+  if (c->abort_dev) cudaFree(c->abort_dev);
+  if (c->err_host) cudaFreeHost(c->err_host);
+  delete c;
+}
+}  // namespace
+
+extern "C" {
+
+const char* lane_allreduce_last_error(lane_comm_t c) {
+  if (!c) return g_init_error.c_str();  // init failures return no comm
+  return c->last_error.c_str();
+}
+
+int lane_allreduce_check(lane_comm_t c) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  if (c->err_host && *(volatile uint32_t*)c->err_host)
+    return fail(c, LANE_ERR_TIMEOUT, "comm: a device-side wait timed out");
+  return LANE_OK;
+}
+
+int lane_allreduce_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, int64_t* chunk_granules,
+                        int64_t* round_granules, int* ctas_per_group, int* launches) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
+    return fail(c, LANE_ERR_UNSUPPORTED, "dtype: unsupported lane_dtype_t");
+  Plan pl;
+  int st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  if (chunk_granules) *chunk_granules = pl.cg;
+  if (round_granules) *round_granules = c->round_cap;
+  if (ctas_per_group) *ctas_per_group = pl.C;
+  if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
+  return LANE_OK;
+}
+
+int lane_topology_query(int nodes, int gpus_per_node, int rank, int* node, int* gpu,
+                        int* group_ranks, int* lane_ranks) {
+  std::string why;
+  int st = validate_topology(nodes, gpus_per_node, 1, &why);
+  if (st != LANE_OK) return st;
+  if (rank < 0 || rank >= nodes * gpus_per_node) return LANE_ERR_INVALID_ARG;
+  const int a = rank / gpus_per_node, g = rank % gpus_per_node;  // p = a*G + g (S L90)
+  if (node) *node = a;
+  if (gpu) *gpu = g;
+  if (group_ranks)
+    for (int h = 0; h < gpus_per_node; ++h) group_ranks[h] = a * gpus_per_node + h;
+  if (lane_ranks)
+    for (int b = 0; b < nodes; ++b) lane_ranks[b] = b * gpus_per_node + g;
+  return LANE_OK;
+}
+
+int lane_partition_query(uint64_t count, int itemsize, int nodes, int gpus_per_node,
+                         int procs_per_gpu, int64_t chunk_granules, int64_t round_granules,
+                         int64_t* units_out, uint64_t max_units, uint64_t* n_units) {
+  std::string why;
+  int st = validate_topology(nodes, gpus_per_node, procs_per_gpu, &why);
+  if (st != LANE_OK) return st;
+  if (itemsize != 2 && itemsize != 4) return LANE_ERR_UNSUPPORTED;
+  const int q = 16 / itemsize;
+  const int64_t ng = (int64_t)((count + q - 1) / q);
+  const int64_t RG = round_granules > 0 ? round_granules : (ng > 0 ? ng : 1);
+  const int N = nodes, G = gpus_per_node, k = procs_per_gpu;
+  auto el = [&](int64_t gr) { return (int64_t)((uint64_t)gr * q < count ? (uint64_t)gr * q : count); };
+  uint64_t n = 0;
+  const int64_t rounds = ng > 0 ? lane::ceil_div(ng, RG) : 0;
+  for (int64_t r = 0; r < rounds; ++r) {
+    const int64_t r0 = r * RG, rlen = (ng - r0) < RG ? (ng - r0) : RG;
+    for (int l = 0; l < k; ++l) {
+      const Span sl = lane::rf_split(rlen, k, l);
+      const int64_t cg = chunk_granules > 0 ? chunk_granules : (sl.len > 0 ? sl.len : 1);
+      const int64_t nc = lane::n_chunks(sl.len, cg);
+      for (int64_t c = 0; c < nc; ++c) {
+        const int64_t c0 = r0 + sl.start + c * cg;
+        const int64_t clen = (sl.len - c * cg) < cg ? (sl.len - c * cg) : cg;
+        for (int g = 0; g < G; ++g) {
+          const Span gp = lane::rf_split(clen, G, g);
+          for (int a = 0; a < N; ++a) {
+            const Span up = lane::rf_split(gp.len, N, a);
+            if (units_out && n < max_units) {
+              int64_t* u = units_out + 9 * n;
+              u[0] = r; u[1] = l; u[2] = c; u[3] = g; u[4] = a;
+              u[5] = el(c0 + gp.start);
+              u[6] = el(c0 + gp.start + gp.len);
+              u[7] = el(c0 + gp.start + up.start);
+              u[8] = el(c0 + gp.start + up.start + up.len);
+            }
+            ++n;
+          }
+        }
+      }
+    }
+  }
+  if (n_units) *n_units = n;
+  return LANE_OK;
+}
+
+}  // extern "C"

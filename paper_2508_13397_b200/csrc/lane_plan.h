@@ -1,0 +1,104 @@
+// lane_plan.h — partition geometry and launch parameters, shared by the host
+// planner (lane_host.cu) and the kernels (lane_kernels.cuh) so that the
+// host-side ownership table tested on CPU is exactly what the device runs.
+//
+// Partition (Alg. 2 c_group/D P L228-240,
+// listing s/PPG at s*l_r P L346-348; remainder-first rule lifted to 16-byte
+// granules, readings R#2-R#4):
+//   message granules -> rounds (fixed size, last smaller)
+//     -> k slices (remainder-first)           : the paper's processes per GPU
+//       -> chunks (fixed CG granules, last smaller) : pipeline unit
+//         -> G group parts (remainder-first)  : phase-1 owner = GPU g
+//           -> N lane sub-parts (remainder-first) : phase-2 owner = node a
+#pragma once
+#include <stdint.h>
+
+#include "../../include/lane_allreduce.h"
+
+#if defined(__CUDACC__)
+#define LANE_HD __host__ __device__ __forceinline__
+#else
+#define LANE_HD inline
+#endif
+
+namespace lane {
+
+constexpr int kGranuleBytes = 16;
+
+struct Span {
+  int64_t start;
+  int64_t len;
+};
+
+// Piece i of `total` split into `parts`, the first total % parts pieces one
+// longer (S L276-278 examples (10,4) -> 3,3,2,2).
+LANE_HD Span rf_split(int64_t total, int64_t parts, int64_t i) {
+  int64_t base = total / parts, rem = total % parts;
+  Span s;
+  s.start = i * base + (i < rem ? i : rem);
+  s.len = base + (i < rem ? 1 : 0);
+  return s;
+}
+
+LANE_HD int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Number of chunks of a slice of `len` granules.
+LANE_HD int64_t n_chunks(int64_t len, int64_t cg) { return len > 0 ? ceil_div(len, cg) : 0; }
+
+// Index of the first chunk of slice l among all chunks of the round
+// (slice-major numbering), O(1).
+LANE_HD int64_t chunk_base(int64_t round_len, int k, int l, int64_t cg) {
+  int64_t base = round_len / k, rem = round_len % k;
+  int64_t big = l < rem ? l : rem;
+  int64_t small = l - big;
+  return big * n_chunks(base + 1, cg) + small * n_chunks(base, cg);
+}
+
+// Total chunks of a round.
+LANE_HD int64_t round_chunks(int64_t round_len, int k, int64_t cg) {
+  return chunk_base(round_len, k, k, cg);
+}
+
+// Per-rank memory as seen from the launching process (peer entries are
+// IPC-mapped UVA addresses; in emulated mode every entry is local).
+struct RankMem {
+  char* s1;          // phase-1 inbox: (G-1) slots x cap chunks x SG granules
+  char* s2;          // phase-2 inbox: N slots x cap chunks x SU granules
+  char* r;           // lane result R: cap chunks x SG granules
+  uint32_t* flags;   // F1[G][cap] F2[N][cap] F3[N][cap] F4[G][cap]
+  const char* send;  // user buffers (only for ranks this launch executes)
+  char* recv;
+};
+
+struct LaneParams {
+  RankMem rk[LANE_MAX_RANKS];
+  int N, G, P, k, C;    // C = CTAs per CTA group (per k-slice)
+  int rank0, nlocal;    // this launch executes ranks rank0 .. rank0+nlocal-1
+  int q;                // elements per granule (16 / itemsize)
+  int tail_elems;       // elements in the message's last granule (q if full)
+  int64_t ng;           // granules of the whole message
+  int64_t round_g0;     // first granule of this round
+  int64_t round_len;    // granules in this round
+  int64_t cg;           // chunk granules
+  int64_t sg, su;       // slot strides (granules): max group part / sub-part
+  int64_t cap;          // chunk capacity (flag and slot stride in chunks)
+  uint32_t epoch;       // monotonically increasing per round, never reset
+  uint32_t pad_;
+  uint64_t timeout_ns;
+  uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
+  uint32_t* abort_flag; // device word: set when any wait of this comm timed out
+};
+
+// Flag indices inside RankMem::flags.
+LANE_HD int64_t f1_idx(const LaneParams& p, int h, int64_t c) { return (int64_t)h * p.cap + c; }
+LANE_HD int64_t f2_idx(const LaneParams& p, int b, int64_t c) {
+  return ((int64_t)p.G + b) * p.cap + c;
+}
+LANE_HD int64_t f3_idx(const LaneParams& p, int b, int64_t c) {
+  return ((int64_t)p.G + p.N + b) * p.cap + c;
+}
+LANE_HD int64_t f4_idx(const LaneParams& p, int h, int64_t c) {
+  return ((int64_t)p.G + 2 * p.N + h) * p.cap + c;
+}
+
+}  // namespace lane

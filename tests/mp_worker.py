@@ -1,0 +1,88 @@
+"""Multi-GPU parity worker: one process per GPU, launched by torchrun.
+
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_worker.py [--quick]
+
+For every virtual layout N x G with N*G == P and several k, dtypes and
+counts, rank p fills its sendbuf with the seeded generator, runs the lane
+allreduce through LaneComm (C ABI, IPC peers over NVLink) and compares its
+output element by element with the CPU oracle (bit-exact). The IPC handle
+exchange uses a gloo process group. Exits non-zero on any mismatch.
+"""
+import argparse
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+import torch.distributed as dist  # noqa: E402
+
+import oracle  # noqa: E402
+import seeded_inputs as si  # noqa: E402
+from seeded_inputs import device as sdev  # noqa: E402
+import paper_2508_13397_b200 as lane  # noqa: E402
+from tests.gpu_util import bits, to_numpy  # noqa: E402
+
+
+def layouts(P):
+    return [(N, P // N) for N in range(1, P + 1) if P % N == 0]
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    args = ap.parse_args()
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    os.environ.setdefault("LANE_TIMEOUT_MS", "10000")
+    os.environ.setdefault("LANE_ROUND_BYTES", str(64 << 20))
+    P = world
+    counts = [1, 7, 4099, (1 << 20) + 3] if args.quick else [1, 7, 64, 4099, (1 << 20) + 3, (1 << 24) + 1]
+    ks = [1, 4] if args.quick else [1, 2, 4, 8]
+    failures = 0
+    t0 = time.time()
+    for N, G in layouts(P):
+        for k in ks:
+            comm = lane.LaneComm(N, G, k, rank=rank, device=local)
+            for dtype in ("int32", "float32", "bfloat16"):
+                tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
+                for it, n in enumerate(counts):
+                    seed = 1000 + 17 * n + k
+                    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", seed, rank)
+                    inplace = it % 2 == 1
+                    out = inp if inplace else torch.empty_like(inp)
+                    comm.allreduce(out, inp)
+                    torch.cuda.synchronize()
+                    comm.check()
+                    if n <= (1 << 20) + 3:
+                        idx = np.arange(n)
+                    else:
+                        idx = si.sample_indices(n, 4099, [n // 2, n // 3])
+                    xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(P)]
+                    ref = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
+                    got = to_numpy(out[torch.from_numpy(idx).cuda()], dtype)
+                    if not np.array_equal(bits(got), bits(ref)):
+                        bad = np.nonzero(bits(got) != bits(ref))[0]
+                        print(f"rank {rank} FAIL {N}x{G} k={k} {dtype} n={n} inplace={inplace}: "
+                              f"{len(bad)} mismatches first {idx[bad[:5]]}", flush=True)
+                        failures += 1
+            dist.barrier()
+            comm.close()
+            dist.barrier()
+    ok = torch.tensor([failures])
+    dist.all_reduce(ok)
+    if rank == 0:
+        print(f"mp_worker P={P}: {'OK' if ok.item() == 0 else 'FAILED'} ({ok.item()} failures) "
+              f"in {time.time() - t0:.1f}s", flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if ok.item() else 0)
+
+
+if __name__ == "__main__":
+    main()

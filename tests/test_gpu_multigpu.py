@@ -1,0 +1,30 @@
+"""Multi-GPU parity (``-m gpu``): torchrun one process per GPU over NVLink.
+
+Skipped when the box has fewer GPUs than the world size under test."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _ngpus():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_multigpu_parity(P):
+    if _ngpus() < P:
+        pytest.skip(f"needs {P} GPUs, have {_ngpus()}")
+    port = 29500 + P
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.join(ROOT, "tests", "mp_worker.py"), "--quick"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert f"mp_worker P={P}: OK" in out, out[-4000:]
