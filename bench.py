@@ -1,0 +1,430 @@
+"""Benchmark of the k-split multi-lane allreduce (arXiv 2508.13397) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W]                 # our arm
+    python bench.py --impl reference ...                                 # CPU oracle arm
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...
+
+Metric (BASELINE.json): allreduce bus GB/s (busbw = S/t * 2(P-1)/P, t =
+device time per call, max over ranks) vs message size at 2/4/8 B200, vs NCCL
+ring, and % of the NVLink roofline.
+
+N = 1: the headline layout (2 virtual nodes x 4 GPUs, k = 1, fp32, 1 GiB per
+rank; BASELINE configs[1] at its largest size) EMULATED on one B200: all 8
+ranks' buffers live in this GPU's HBM and one cooperative launch of the same
+kernel runs every rank (lane_allreduce_emulated). The bound is then HBM.
+N > 1: one process per GPU (torchrun), real IPC/NVLink; default layout
+2 x (N/2) virtual nodes, k = 1, fp32, 1 GiB per rank. Bound: NVLink.
+
+One JSON line is printed by rank 0. Each timed step is one lane_allreduce call
+(one kernel launch per round; one round at these sizes) on inputs already in
+HBM; inputs are 1 GiB per rank (> 126 MB L2), so no L2 flush is needed.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+# NCCL is used ONLY for the timed comparator; the required comparator is ring.
+os.environ.setdefault("NCCL_ALGO", "Ring")
+
+METRIC = "allreduce bus GB/s vs msg size at 2/4/8 B200 vs NCCL ring; % of NVLink roofline"
+NVLINK_PEAK = 770.0  # GB/s per direction per GPU, measured peer copy (B200_PROFILING.md)
+NVLINK_NOMINAL = 900.0
+TDT = {"int32": "int32", "float32": "float32", "bfloat16": "bfloat16"}
+SHORT = {"int32": "i32", "float32": "f32", "bfloat16": "bf16"}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="lane", choices=["lane", "reference"])
+    ap.add_argument("--layout", default=None, help="NxG virtual layout (default 2x4 / 2x(N/2))")
+    ap.add_argument("--k", type=int, default=1, help="procs per GPU = CTA groups")
+    ap.add_argument("--dtype", default="float32", choices=list(TDT))
+    ap.add_argument("--mib", type=float, default=1024.0, help="message MiB per rank")
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-nccl", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------- helpers
+def itemsize(dtype):
+    return 2 if dtype == "bfloat16" else 4
+
+
+def busbw(bytes_, P, ms):
+    return bytes_ * 2 * (P - 1) / P / (ms * 1e-3) / 1e9 if P > 1 else bytes_ / (ms * 1e-3) / 1e9
+
+
+class Clocks:
+    """nvidia-smi sampler running while the timed region runs."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpus):
+        self.gpus = gpus
+        self.proc = None
+        self.out = os.path.join("/tmp", f"lane_clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        try:
+            self.f = open(self.out, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100",
+                 "-i", ",".join(str(g) for g in self.gpus)], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+            self.f.close()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        try:
+            for line in open(self.out):
+                f = [x.strip() for x in line.split(",")]
+                if len(f) < 8:
+                    continue
+                try:
+                    sm.append(float(f[1]))
+                    mx.append(float(f[2]))
+                except ValueError:
+                    continue
+                for nm, v in zip(names, f[4:8]):
+                    if v.lower().startswith("active"):
+                        reasons.add(nm)
+        except OSError:
+            pass
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def device_time_ms(fn, steps, warmup, stream, barrier=None):
+    import torch
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        fn()
+    e.record(stream)
+    torch.cuda.synchronize()
+    if barrier:
+        barrier()
+    return s.elapsed_time(e) / steps
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
+
+
+def cpu_baseline(N, G, k, dtype, seconds):
+    """The oracle as it stands, on this host, single-threaded numpy, on a
+    bounded sample of the workload (same layout/dtype, 2^20 elements per rank)."""
+    import oracle
+    import seeded_inputs as si
+    n = 1 << 20
+    xs = si.generate_all(dtype, "signed", 42, N * G, n)
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        oracle.lane_allreduce(xs, N, G, k, dtype)
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 200:
+            break
+    t = el / reps
+    S = n * itemsize(dtype)
+    return {"value": round(busbw(S, N * G, t * 1e3), 4), "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "host_cores": os.cpu_count(),
+            "sample": f"{N}x{G} k={k} {dtype}, {n} elements ({S >> 20} MiB) per simulated rank, "
+                      f"{reps} reps in {el:.1f}s, {t * 1e3:.1f} ms per oracle allreduce (numpy, 1 thread)"}
+
+
+def sample_check(outs, N, G, dtype, n, seed, ranks):
+    """Bit-exact check of sampled outputs against the oracle."""
+    import numpy as np
+    import torch
+    import oracle
+    import seeded_inputs as si
+    idx = si.sample_indices(n, 65537, [n // 2, n // 3, n // 5])
+    it = torch.from_numpy(idx).to(outs[0].device)
+    xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(N * G)]
+    ref = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
+    vb = np.uint16 if dtype == "bfloat16" else np.uint32
+    for o in outs:
+        t = o[it].cpu()
+        got = (t.view(torch.int16).numpy() if dtype == "bfloat16" else t.view(torch.int32).numpy()).view(vb)
+        if not np.array_equal(got, ref.view(vb)):
+            return False
+    return True
+
+
+def base_line(args, N_gpus, K, W):
+    return {"metric": METRIC, "unit": "GB/s", "n_gpus": N_gpus, "steps": K, "warmup": W,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": SHORT[args.dtype]}
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle
+    import seeded_inputs as si
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
+    N, G = layout_for(args, max(world, args.gpus))
+    n = 1 << 18  # bounded sample per rank per step
+    xs = si.generate_all(args.dtype, "signed", 42, N * G, n)
+    for _ in range(args.warmup):
+        oracle.lane_allreduce(xs, N, G, args.k, args.dtype)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.lane_allreduce(xs, N, G, args.k, args.dtype)
+    t = (time.perf_counter() - t0) / args.steps
+    S = n * itemsize(args.dtype)
+    v = round(busbw(S, N * G, t * 1e3), 4)
+    line = base_line(args, args.gpus, args.steps, args.warmup)
+    line.update({"impl": "reference", "value": v, "ms_per_step": round(t * 1e3, 3),
+                 "data": "synthetic (seeded counter hash)",
+                 "config": {"workload": f"CPU oracle, {N}x{G} virtual ranks, k={args.k}, {args.dtype}, "
+                                        f"{S >> 10} KiB per rank per step (bounded sample of the "
+                                        f"{int(args.mib)} MiB workload)",
+                            "layout": f"{N}x{G}", "procs_per_gpu": args.k},
+                 "cpu_baseline": {"value": v, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                                  "host_cores": os.cpu_count(),
+                                  "sample": f"{n} elements per simulated rank per step"},
+                 "e2e": {"value": v, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                 "gpu_launches": 0})
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def layout_for(args, P):
+    if args.layout:
+        N, G = map(int, args.layout.lower().split("x"))
+        return N, G
+    if P == 1:
+        return 2, 4  # emulated headline layout
+    if P % 2 == 0:
+        return 2, P // 2
+    return P, 1
+
+
+# ----------------------------------------------------------------- N = 1 (emulated)
+def run_single(args):
+    import torch
+    import paper_2508_13397_b200 as lane
+    from seeded_inputs import device as sdev
+    N, G = layout_for(args, 1)
+    P, k, dtype = N * G, args.k, args.dtype
+    isz = itemsize(dtype)
+    n = int(args.mib * (1 << 20)) // isz
+    S = n * isz
+    torch.cuda.set_device(0)
+    tdt = getattr(torch, dtype)
+    emu = lane.LaneEmulator(N, G, k, device=0)
+    plan = emu.plan(n, dtype)
+    seed = 42
+    ins = [sdev.fill(torch.empty(n, dtype=tdt, device="cuda:0"), dtype, "signed", seed, p) for p in range(P)]
+    outs = [torch.empty_like(t) for t in ins]
+    stream = torch.cuda.current_stream()
+    step = lambda: emu.allreduce(outs, ins)  # noqa: E731
+    with Clocks([0]) as clk:
+        ms = device_time_ms(step, args.steps, args.warmup, stream)
+    emu.check()
+    ok = sample_check(outs, N, G, dtype, n, seed, range(P))
+    # roofline: HBM. Algorithmic bytes per launch = every rank's input read
+    # once + output written once (2*P*S), the compulsory traffic of an
+    # allreduce whose P buffers share one HBM.
+    pk = peaks()
+    hbm_peak = float(pk.get("hbm_gbs", 6650.0))
+    launches = max(plan["launches"], 1)
+    achieved = 2 * P * S / (ms / launches * 1e-3) / 1e9
+    line = base_line(args, 1, args.steps, args.warmup)
+    bw = busbw(S, P, ms)
+    line.update({
+        "value": round(bw, 2) if ok else None, "ms_per_step": round(ms, 4),
+        "data": "synthetic (seeded counter hash; signed values)",
+        "config": {"workload": f"{N}x{G} virtual ranks emulated on 1 B200 (all ranks in one cooperative "
+                               f"launch), k={k}, {dtype}, {S >> 20} MiB per rank (BASELINE configs[1] layout "
+                               f"at its largest size)",
+                   "layout": f"{N}x{G}", "procs_per_gpu": k, "bytes_per_rank": S, "emulated": True,
+                   "l2": "inputs larger than L2 (8 x 1 GiB)", "plan": plan},
+        "algbw": round(S / (ms * 1e-3) / 1e9, 2),
+        "verified": ok,
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback guide",
+                     "algorithmic_bytes_per_launch": 2 * P * S},
+        "gpu_launches": args.steps * launches,
+        "clocks": clk.summary(),
+    })
+    if not args.no_e2e:
+        line["e2e"] = e2e_single(emu, ins, outs, N, G, dtype, n, S, args)
+    if not args.no_cpu:
+        line["cpu_baseline"] = cpu_baseline(N, G, k, dtype, args.cpu_seconds)
+    print(json.dumps(line), flush=True)
+    return 0 if ok else 1
+
+
+def e2e_single(emu, ins, outs, N, G, dtype, n, S, args):
+    import torch
+    P = N * G
+    h_in = [torch.empty(n, dtype=ins[0].dtype).pin_memory() for _ in range(P)]
+    h_out = [torch.empty(n, dtype=ins[0].dtype).pin_memory() for _ in range(P)]
+    for h, d in zip(h_in, ins):
+        h.copy_(d)
+    stream = torch.cuda.current_stream()
+    step = lambda: emu.allreduce_host(h_out, h_in)  # noqa: E731  (H2D + kernel + D2H, then sync)
+    ms = device_time_ms(step, args.e2e_steps, 1, stream)
+    return {"value": round(busbw(S, P, ms), 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
+            "h2d_bytes_per_step": P * S, "d2h_bytes_per_step": P * S,
+            "api": "lane_allreduce_emulated_host (C ABI, pinned host buffers)"}
+
+
+# ----------------------------------------------------------------- N > 1
+def run_multi(args):
+    import torch
+    import torch.distributed as dist
+    import paper_2508_13397_b200 as lane
+    from seeded_inputs import device as sdev
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("cpu:gloo,cuda:nccl")
+    N, G = layout_for(args, world)
+    if N * G != world:
+        raise SystemExit(f"layout {N}x{G} does not match world size {world}")
+    P, k, dtype = world, args.k, args.dtype
+    isz = itemsize(dtype)
+    n = int(args.mib * (1 << 20)) // isz
+    S = n * isz
+    tdt = getattr(torch, dtype)
+    comm = lane.LaneComm(N, G, k, rank=rank, device=local)
+    plan = comm.plan(n, dtype)
+    seed = 42
+    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", seed, rank)
+    out = torch.empty_like(inp)
+    stream = torch.cuda.current_stream()
+    barrier = lambda: dist.barrier()  # noqa: E731
+    step = lambda: comm.allreduce(out, inp)  # noqa: E731
+    clk = Clocks(list(range(world))) if rank == 0 else None
+    if clk:
+        clk.__enter__()
+    ms = device_time_ms(step, args.steps, args.warmup, stream, barrier)
+    if clk:
+        clk.__exit__()
+    comm.check()
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    ok = sample_check([out], N, G, dtype, n, seed, [rank])
+    okt = torch.tensor([0 if ok else 1])
+    dist.all_reduce(okt)
+    ok = okt.item() == 0
+    bw = busbw(S, P, ms_max)
+    launches = max(plan["launches"], 1)
+    line = base_line(args, world, args.steps, args.warmup)
+    line.update({
+        "value": round(bw, 2) if ok else None, "ms_per_step": round(ms_max, 4),
+        "data": "synthetic (seeded counter hash; signed values)",
+        "config": {"workload": f"{N}x{G} virtual nodes on {world} B200 (one process per GPU, IPC peers over "
+                               f"NVLink 5), k={k}, {dtype}, {S >> 20} MiB per rank",
+                   "layout": f"{N}x{G}", "procs_per_gpu": k, "bytes_per_rank": S, "emulated": False,
+                   "l2": "inputs larger than L2 (1 GiB per rank)", "plan": plan},
+        "algbw": round(S / (ms_max * 1e-3) / 1e9, 2),
+        "verified": ok,
+        "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
+                     "frac": round(bw / NVLINK_PEAK, 4), "frac_of_nominal_900": round(bw / NVLINK_NOMINAL, 4),
+                     "traffic": None,
+                     "peak_source": "measured peer copy per direction, B200_PROFILING.md (no NVLink entry in "
+                                    "MEASURED_PEAKS.json)",
+                     "algorithmic_bytes_per_launch": int(2 * (P - 1) / P * S / launches)},
+        "gpu_launches": args.steps * launches,
+    })
+    if clk:
+        line["clocks"] = clk.summary()
+    if not args.no_e2e:
+        line["e2e"] = e2e_multi(comm, inp, N, G, dtype, n, S, args, dist)
+    if not args.no_nccl:
+        line["nccl_ring"] = nccl_ring(inp, S, P, args, dist, stream)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+def e2e_multi(comm, inp, N, G, dtype, n, S, args, dist):
+    import torch
+    h_in = torch.empty(n, dtype=inp.dtype).pin_memory()
+    h_in.copy_(inp)
+    h_out = torch.empty_like(h_in).pin_memory()
+    stream = torch.cuda.current_stream()
+    ms = device_time_ms(lambda: comm.allreduce_host(h_out, h_in), args.e2e_steps, 1, stream,
+                        lambda: dist.barrier())
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    P = N * G
+    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 3),
+            "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+            "api": "lane_allreduce_host (C ABI, pinned host buffers)"}
+
+
+def nccl_ring(inp, S, P, args, dist, stream):
+    import torch
+    buf = inp.clone()
+    step = lambda: dist.all_reduce(buf)  # noqa: E731
+    ms = device_time_ms(step, args.steps, args.warmup, stream, lambda: dist.barrier())
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 4),
+            "algo": os.environ.get("NCCL_ALGO", "default"), "version": ".".join(map(str, torch.cuda.nccl.version()))}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return run_multi(args)
+    if args.gpus > 1:
+        raise SystemExit("--gpus > 1 must be launched with torchrun (one process per GPU)")
+    return run_single(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
