@@ -22,6 +22,7 @@
 
 #include "../../include/lane_allreduce.h"
 #include "lane_kernels.cuh"
+#include "lane_tma.cuh"
 #include "lane_plan.h"
 
 using lane::LaneParams;
@@ -59,6 +60,7 @@ struct lane_comm_s {
   bool emulated = false;
   bool connected = false;
   int threads = 512;
+  int engine = 1;           // 0 = LSU (ld/st.global), 1 = TMA bulk pipeline
   int ctas_per_group = 0;  // 0 = choose per call
   int max_coresident = 0;  // CTAs of the kernel that fit on the device at once
   int sm_count = 0;
@@ -142,9 +144,16 @@ void carve(lane_comm_t c, char* base, RankMem* m) {
 }
 
 template <int DT>
-int occupancy_of(int threads) {
+int occupancy_of(int engine, int threads) {
   int nb = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::lane_allreduce_kernel<DT>, threads, 0);
+  if (engine == 1) {
+    cudaFuncSetAttribute(lane::tma::lane_tma_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         lane::tma::kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::tma::lane_tma_kernel<DT>, lane::tma::kThreads,
+                                                  lane::tma::kSmemBytes);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::lane_allreduce_kernel<DT>, threads, 0);
+  }
   return nb;
 }
 
@@ -159,11 +168,15 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->device = device;
   c->emulated = emulated;
   c->threads = (int)env_i64("LANE_THREADS", 512);
+  {
+    const char* e = getenv("LANE_ENGINE");
+    c->engine = (e && strcmp(e, "lsu") == 0) ? 0 : 1;
+  }
   if (c->threads < 64 || c->threads > 512 || c->threads % 32)
     return fail(c, LANE_ERR_INVALID_ARG, "LANE_THREADS must be a multiple of 32 in [64, 512]");
   c->ctas_per_group = (int)env_i64("LANE_CTAS_PER_GROUP", 0);
   c->round_cap = env_i64("LANE_ROUND_BYTES", (int64_t)1 << 30) / 16;
-  c->cg_max = env_i64("LANE_CHUNK_BYTES", 256 << 10) / 16;
+  c->cg_max = env_i64("LANE_CHUNK_BYTES", 1 << 20) / 16;
   c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 16 << 10) / 16;
   if (c->round_cap < 1024) return fail(c, LANE_ERR_INVALID_ARG, "LANE_ROUND_BYTES must be >= 16 KiB");
   if (c->cg_min < 16) c->cg_min = 16;
@@ -173,8 +186,8 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
 
   LANE_CUDA(c, cudaSetDevice(device));
   LANE_CUDA(c, cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
-  int occ = occupancy_of<0>(c->threads);
-  int o1 = occupancy_of<1>(c->threads), o2 = occupancy_of<2>(c->threads);
+  int occ = occupancy_of<0>(c->engine, c->threads);
+  int o1 = occupancy_of<1>(c->engine, c->threads), o2 = occupancy_of<2>(c->engine, c->threads);
   occ = occ < o1 ? occ : o1;
   occ = occ < o2 ? occ : o2;
   if (occ < 1) occ = 1;
@@ -248,9 +261,9 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   int ranks_here = c->emulated ? c->P : 1;
   int C = c->ctas_per_group;
   if (C <= 0) {
-    int budget = c->emulated ? c->max_coresident : (int)env_i64("LANE_CTAS_TOTAL", 64);
+    int budget = c->emulated ? c->max_coresident : (int)env_i64("LANE_CTAS_TOTAL", c->sm_count);
+    if (budget > c->max_coresident) budget = c->max_coresident;
     C = budget / (ranks_here * c->k);
-    if (C > 64) C = 64;
   }
   if (C < 1) C = 1;
   if ((int64_t)C * c->k * ranks_here > c->max_coresident)
@@ -296,16 +309,25 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
     if (p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
     p.epoch = ++c->epoch;
-    dim3 grid((unsigned)(nlocal * c->k * p.C)), block((unsigned)c->threads);
+    const bool tma = c->engine == 1;
+    dim3 grid((unsigned)(nlocal * c->k * p.C));
+    dim3 block((unsigned)(tma ? lane::tma::kThreads : c->threads));
+    const size_t smem = tma ? (size_t)lane::tma::kSmemBytes : 0;
     cudaError_t e;
     void* args[] = {&p};
-    const void* fn = dtype == LANE_INT32     ? (const void*)lane::lane_allreduce_kernel<0>
-                     : dtype == LANE_FLOAT32 ? (const void*)lane::lane_allreduce_kernel<1>
-                                             : (const void*)lane::lane_allreduce_kernel<2>;
-    if (c->emulated)
-      e = cudaLaunchCooperativeKernel(fn, grid, block, args, 0, s);
+    const void* fn;
+    if (tma)
+      fn = dtype == LANE_INT32     ? (const void*)lane::tma::lane_tma_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::tma::lane_tma_kernel<1>
+                                   : (const void*)lane::tma::lane_tma_kernel<2>;
     else
-      e = cudaLaunchKernel(fn, grid, block, args, 0, s);
+      fn = dtype == LANE_INT32     ? (const void*)lane::lane_allreduce_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::lane_allreduce_kernel<1>
+                                   : (const void*)lane::lane_allreduce_kernel<2>;
+    if (c->emulated)
+      e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s);
+    else
+      e = cudaLaunchKernel(fn, grid, block, args, smem, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "lane_allreduce_kernel launch");
   }
   return LANE_OK;
