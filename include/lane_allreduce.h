@@ -138,6 +138,15 @@ const char* lane_allreduce_last_error(lane_comm_t comm);
  * LANE_OK or LANE_ERR_TIMEOUT. Does not synchronize. */
 int lane_allreduce_check(lane_comm_t comm);
 
+/* Per-CTA stall accounting of the last launch (TMA engine), enabled by
+ * creating the comm with LANE_TRACE=1: 16 uint64 per CTA (field order in
+ * producer total / flag wait / empty wait / tiles,
+ * storer total / full wait / sync / read wait / flush / jobs, per-phase
+ * A..E time, bytes stored; nanoseconds). Synchronizes the device. Writes at
+ * most max_words to out (may be NULL) and the available count to *n_words.
+ * INVALID_ARG if tracing is off. */
+int lane_allreduce_trace(lane_comm_t comm, uint64_t* out, size_t max_words, size_t* n_words);
+
 /* The execution plan lane_allreduce uses for (count, dtype): chunk size and
  * round size in 16-byte granules, CTAs per CTA group, kernel launches
  * (rounds) per call. Any out-pointer may be NULL. */

@@ -89,6 +89,21 @@ class _CommBase:
         return {"chunk_granules": cg.value, "round_granules": rg.value, "ctas_per_group": C.value,
                 "launches": launches.value}
 
+    TRACE_FIELDS = ("prod_total", "prod_flag_wait", "prod_empty_wait", "prod_tiles", "store_total",
+                    "store_full_wait", "store_sync", "store_read_wait", "store_flush", "store_jobs",
+                    "phase_A", "phase_B", "phase_C", "phase_D", "phase_E", "bytes_stored")
+
+    def trace(self) -> list:
+        """Per-CTA stall accounting of the last launch (needs LANE_TRACE=1 at
+        construction): list of dicts, nanoseconds."""
+        lib = _lib.load()
+        n = ctypes.c_size_t()
+        _lib.check(lib.lane_allreduce_trace(self._comm, None, 0, ctypes.byref(n)), self._comm)
+        buf = (ctypes.c_uint64 * max(n.value, 1))()
+        _lib.check(lib.lane_allreduce_trace(self._comm, buf, n.value, ctypes.byref(n)), self._comm)
+        w = len(self.TRACE_FIELDS)
+        return [dict(zip(self.TRACE_FIELDS, list(buf)[i * w:(i + 1) * w])) for i in range(n.value // w)]
+
     def check(self) -> None:
         _lib.check(_lib.load().lane_allreduce_check(self._comm), self._comm)
 

@@ -56,6 +56,7 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_finalize": (I, [P]),
         "lane_allreduce_last_error": (ctypes.c_char_p, [P]),
         "lane_allreduce_check": (I, [P]),
+        "lane_allreduce_trace": (I, [P, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)]),
         "lane_allreduce_plan": (I, [P, SZ, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_topology_query": (I, [I, I, I, ctypes.POINTER(I), ctypes.POINTER(I),

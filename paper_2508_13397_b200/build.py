@@ -22,8 +22,8 @@ TARGETS = [
     {
         "out": os.path.join(PKG, "liblane_allreduce.so"),
         "srcs": [os.path.join(PKG, "csrc", "lane_host.cu")],
-        "deps": [os.path.join(PKG, "csrc", f) for f in ("lane_plan.h", "lane_kernels.cuh")]
-        + [os.path.join(ROOT, "include", "lane_allreduce.h")],
+        "deps": [os.path.join(PKG, "csrc", f) for f in sorted(os.listdir(os.path.join(PKG, "csrc")))
+                 if f.endswith((".h", ".cuh"))] + [os.path.join(ROOT, "include", "lane_allreduce.h")],
         "log": os.path.join(PKG, "csrc", "ptxas_lane_allreduce.log"),
     },
     {

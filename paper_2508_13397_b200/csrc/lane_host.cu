@@ -61,6 +61,7 @@ struct lane_comm_s {
   bool connected = false;
   int threads = 512;
   int engine = 1;           // 0 = LSU (ld/st.global), 1 = TMA bulk pipeline
+  bool lsu_store = true;    // TMA engine: consumers store with st.global (else bulk stores)
   int ctas_per_group = 0;  // 0 = choose per call
   int max_coresident = 0;  // CTAs of the kernel that fit on the device at once
   int sm_count = 0;
@@ -77,6 +78,8 @@ struct lane_comm_s {
   uint32_t* err_dev = nullptr;
   uint32_t* abort_dev = nullptr;
   uint64_t timeout_ns = 0;
+  uint64_t* trace = nullptr;  // LANE_TRACE=1: kTraceWords per CTA of the last launch
+  int trace_ctas = 0;
   std::vector<char*> stage;  // device staging for the host-buffer API
   uint64_t stage_bytes = 0;
   std::string last_error;
@@ -147,9 +150,11 @@ template <int DT>
 int occupancy_of(int engine, int threads) {
   int nb = 0;
   if (engine == 1) {
-    cudaFuncSetAttribute(lane::tma::lane_tma_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(lane::tma::lane_tma_kernel<DT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          lane::tma::kSmemBytes);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::tma::lane_tma_kernel<DT>, lane::tma::kThreads,
+    cudaFuncSetAttribute(lane::tma::lane_tma_kernel<DT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         lane::tma::kSmemBytes);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::tma::lane_tma_kernel<DT, true>, lane::tma::kThreads,
                                                   lane::tma::kSmemBytes);
   } else {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::lane_allreduce_kernel<DT>, threads, 0);
@@ -171,6 +176,8 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   {
     const char* e = getenv("LANE_ENGINE");
     c->engine = (e && strcmp(e, "lsu") == 0) ? 0 : 1;
+    const char* st = getenv("LANE_STORE");
+    c->lsu_store = !(st && strcmp(st, "bulk") == 0);
   }
   if (c->threads < 64 || c->threads > 512 || c->threads % 32)
     return fail(c, LANE_ERR_INVALID_ARG, "LANE_THREADS must be a multiple of 32 in [64, 512]");
@@ -206,6 +213,10 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   LANE_CUDA(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   LANE_CUDA(c, cudaMalloc(&c->abort_dev, 64));
   LANE_CUDA(c, cudaMemset(c->abort_dev, 0, 64));
+  if (env_i64("LANE_TRACE", 0)) {
+    LANE_CUDA(c, cudaMalloc(&c->trace, (size_t)c->max_coresident * lane::kTraceWords * 8));
+    LANE_CUDA(c, cudaMemset(c->trace, 0, (size_t)c->max_coresident * lane::kTraceWords * 8));
+  }
   LANE_CUDA(c, cudaDeviceSynchronize());
   if (emulated) {
     for (int p = 0; p < c->P; ++p) carve(c, c->own[p], &c->rk[p]);
@@ -297,6 +308,7 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.timeout_ns = c->timeout_ns;
   p.err = c->err_dev;
   p.abort_flag = c->abort_dev;
+  p.trace = c->trace;
   return p;
 }
 
@@ -311,15 +323,20 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
+    c->trace_ctas = (int)grid.x;
     dim3 block((unsigned)(tma ? lane::tma::kThreads : c->threads));
     const size_t smem = tma ? (size_t)lane::tma::kSmemBytes : 0;
     cudaError_t e;
     void* args[] = {&p};
     const void* fn;
-    if (tma)
-      fn = dtype == LANE_INT32     ? (const void*)lane::tma::lane_tma_kernel<0>
-           : dtype == LANE_FLOAT32 ? (const void*)lane::tma::lane_tma_kernel<1>
-                                   : (const void*)lane::tma::lane_tma_kernel<2>;
+    if (tma && c->lsu_store)
+      fn = dtype == LANE_INT32     ? (const void*)lane::tma::lane_tma_kernel<0, true>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::tma::lane_tma_kernel<1, true>
+                                   : (const void*)lane::tma::lane_tma_kernel<2, true>;
+    else if (tma)
+      fn = dtype == LANE_INT32     ? (const void*)lane::tma::lane_tma_kernel<0, false>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::tma::lane_tma_kernel<1, false>
+                                   : (const void*)lane::tma::lane_tma_kernel<2, false>;
     else
       fn = dtype == LANE_INT32     ? (const void*)lane::lane_allreduce_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::lane_allreduce_kernel<1>
@@ -592,6 +609,7 @@ void release(lane_comm_t c) {
   for (char* p : c->own) cudaFree(p);
   for (char* p : c->stage) cudaFree(p);
   if (c->abort_dev) cudaFree(c->abort_dev);
+  if (c->trace) cudaFree(c->trace);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;
 }
@@ -602,6 +620,19 @@ extern "C" {
 const char* lane_allreduce_last_error(lane_comm_t c) {
   if (!c) return g_init_error.c_str();  // init failures return no comm
   return c->last_error.c_str();
+}
+
+int lane_allreduce_trace(lane_comm_t c, uint64_t* out, size_t max_words, size_t* n_words) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  if (!c->trace) return fail(c, LANE_ERR_INVALID_ARG, "trace: comm was created without LANE_TRACE=1");
+  const size_t n = (size_t)c->trace_ctas * lane::kTraceWords;
+  if (n_words) *n_words = n;
+  if (out && max_words) {
+    LANE_CUDA(c, cudaSetDevice(c->device));
+    LANE_CUDA(c, cudaDeviceSynchronize());
+    LANE_CUDA(c, cudaMemcpy(out, c->trace, (max_words < n ? max_words : n) * 8, cudaMemcpyDeviceToHost));
+  }
+  return LANE_OK;
 }
 
 int lane_allreduce_check(lane_comm_t c) {

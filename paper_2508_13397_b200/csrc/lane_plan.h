@@ -87,6 +87,15 @@ struct LaneParams {
   uint64_t timeout_ns;
   uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
   uint32_t* abort_flag; // device word: set when any wait of this comm timed out
+  uint64_t* trace;      // optional per-CTA stall accounting (LANE_TRACE=1), else null
+};
+
+// Trace record layout (kTraceWords uint64 per CTA, nanoseconds unless noted).
+enum TraceField {
+  kTrProdTotal = 0, kTrProdFlagWait, kTrProdEmptyWait, kTrProdTiles,
+  kTrStoreTotal, kTrStoreFullWait, kTrStoreSync, kTrStoreReadWait, kTrStoreFlush, kTrStoreJobs,
+  kTrPhaseA, kTrPhaseB, kTrPhaseC, kTrPhaseD, kTrPhaseE, kTrBytes,
+  kTraceWords
 };
 
 // Flag indices inside RankMem::flags.

@@ -24,10 +24,11 @@
 //                    frees ring stages, and after a job completes
 //                    (wait_group 0) releases its flags with st.release.sys.
 //
-// Schedule: CTA j of CTA group l owns chunks j, j+C, ... of slice l; at
-// step s it runs A(c_s), B(c_{s-1}), C(c_{s-2}), D(c_{s-3}), E(c_{s-4}) — a
-// wavefront, so every wait is on work the peer's CTA j did one step earlier
-// and each step mixes push, pull and local traffic.
+// Schedule: CTA j of CTA group l owns chunks j, j+C, ... of slice l. The
+// producer issues jobs OUT OF ORDER: it takes the next job of any phase whose
+// flags are already set (per chunk, phases stay in order A..E; phase A runs at
+// most a small window of chunks ahead), so one lagging peer does not stall
+// the ring. Consumers are driven entirely by per-stage tile descriptors.
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -41,11 +42,12 @@ namespace tma {
 constexpr int kStages = 4;
 constexpr int kStageBytes = 48 * 1024;
 constexpr int kStageGranules = kStageBytes / 16;
-constexpr int kConsumerWarps = 7;
-constexpr int kThreads = 32 * (1 + kConsumerWarps);
+constexpr int kConsumerWarps = 6;
+constexpr int kThreads = 32 * (2 + kConsumerWarps);  // producer warp, releaser warp, consumers
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + 16;
+constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 256 + kRelSlots * 136 + 64;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -98,7 +100,9 @@ __device__ __forceinline__ void consumers_sync() {
 }
 
 // ------------------------------------------------------------------ jobs
+// ------------------------------------------------------------------ jobs
 struct Job {
+  int ph;                           // 0..4 = phase A..E
   int nsrc, ndst, x_src, recv_dst;  // x_src / recv_dst: index or -1
   int nwait, nrel;
   int64_t len;  // granules
@@ -116,10 +120,13 @@ struct Ctx {
   Msg msg;
 };
 
+// Jobs per chunk of each phase. With G == 1 the phase-1 sum of the own lane
+// sub-part is the sendbuf itself, so B only sends the N-1 remote sub-parts and
+// C reads its own term straight from sendbuf.
 __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
   switch (ph) {
     case 0: return x.G - 1;
-    case 1: return x.N;
+    case 1: return x.G == 1 ? x.N - 1 : x.N;
     case 2: return x.N > 1 ? 1 : 0;
     case 3: return x.N - 1;
     default: return x.G - 1;
@@ -130,6 +137,7 @@ __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
 __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
   const LaneParams& p = *x.p;
   const int a = x.a, g = x.g, N = x.N, G = x.G;
+  J.ph = ph;
   J.nsrc = 1;
   J.ndst = 1;
   J.x_src = -1;
@@ -148,7 +156,7 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
     J.dst[0] = s1_slot(p, dm, g < gd ? g : g - 1, ch.id);
     J.rel[J.nrel++] = dm.flags + f1_idx(p, g, ch.id);
   } else if (ph == 1) {  // B: reduce part g over the node, sub-part b
-    const int b = (a + 1 + t) % N;  // own sub-part last
+    const int b = (a + 1 + t) % N;  // own sub-part last (absent when G == 1)
     const Span up = rf_split(gp.len, N, b);
     J.len = up.len;
     J.m0 = ch.g0 + gp.start + up.start;
@@ -171,14 +179,19 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
       for (int h = 0; h < G; ++h)
         if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
     }
-  } else if (ph == 2) {  // C: reduce my sub-part over the lane
+  } else if (ph == 2) {  // C: reduce my sub-part over the lane (ascending b)
     const Span up = rf_split(gp.len, N, a);
     J.len = up.len;
     J.m0 = ch.g0 + gp.start + up.start;
     J.nsrc = N;
     for (int b = 0; b < N; ++b) {
-      J.src[b] = s2_slot(p, *x.me, b, ch.id);
-      J.wait[J.nwait++] = x.me->flags + f2_idx(p, b, ch.id);
+      if (G == 1 && b == a) {
+        J.src[b] = x.msg.send + J.m0;  // T1 of a single-GPU node is its sendbuf
+        J.x_src = b;
+      } else {
+        J.src[b] = s2_slot(p, *x.me, b, ch.id);
+        J.wait[J.nwait++] = x.me->flags + f2_idx(p, b, ch.id);
+      }
     }
     J.ndst = 2;
     J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
@@ -198,7 +211,7 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
       J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
       J.dst[1] = x.msg.recv + J.m0;
       J.recv_dst = 1;
-      if (t == N - 2)
+      if (t == N - 2)  // R of part g complete (C's and every D's stores precede this)
         for (int h = 0; h < G; ++h)
           if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
     } else {
@@ -220,62 +233,57 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
 __device__ __forceinline__ int64_t tile_granules(int nsrc) {
   return (int64_t)(kStageGranules / nsrc);
 }
-__device__ __forceinline__ int64_t n_tiles(const Job& J) {
-  const int64_t T = tile_granules(J.nsrc);
-  return J.len > 0 ? (J.len + T - 1) / T : 1;  // empty jobs still take one (empty) tile
+
+// Descriptor of one ring stage, written by the producer before it arrives on
+// the stage's "full" barrier; consumers need nothing else.
+struct TileDesc {
+  int nsrc;       // 0 = end of the CTA's work
+  int ndst, recv_dst, nrel, ph;
+  int64_t T;      // slot stride in granules
+  int64_t tl;     // granules in this tile
+  int64_t poff;   // granule offset of the message's partial last granule in the tile, or -1
+  uint4* dst[2];  // already offset to the tile start
+  uint32_t* rel[kMaxSrc];  // flags to release once this tile (the job's last) is stored
+};
+
+static_assert(sizeof(TileDesc) <= 256, "TileDesc must fit its smem slot");
+
+// A job's flag releases, handed from the storer to the releaser warp.
+struct RelRec {
+  int n;
+  uint32_t* f[kMaxSrc];
+};
+static_assert(sizeof(RelRec) <= 136, "RelRec must fit its smem slot");
+
+struct RelRing {
+  volatile int tail;  // records published by the storer
+  volatile int head;  // records retired by the releaser
+  volatile int done;  // storer finished (or aborted)
+};
+
+__device__ __forceinline__ bool flag_ready(const LaneParams& p, const uint32_t* f) {
+  return (int32_t)(ld_acquire_sys(f) - p.epoch) >= 0;
 }
 
-// Acquire-wait one flag (producer thread). false on timeout / abort.
-__device__ bool wait_one(const LaneParams& p, const uint32_t* f) {
-  if ((int32_t)(ld_acquire_sys(f) - p.epoch) >= 0) return true;
-  const uint64_t t0 = globaltimer_ns();
-  for (uint32_t it = 1;; ++it) {
-    if ((int32_t)(ld_acquire_sys(f) - p.epoch) >= 0) return true;
-    if ((it & 63u) == 0) {
-      if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) return false;
-      if (globaltimer_ns() - t0 > p.timeout_ns) {
-        atomicExch(p.abort_flag, 1u);
-        *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_TIMEOUT);
-        __threadfence_system();
-        return false;
-      }
-    }
-  }
+__device__ __forceinline__ ChunkGeo chunk_geo(const LaneParams& p, int64_t cb, const Span& sl, int64_t c) {
+  ChunkGeo ch;
+  ch.id = cb + c;
+  ch.g0 = p.round_g0 + sl.start + c * p.cg;
+  const int64_t rest = sl.len - c * p.cg;
+  ch.len = rest < p.cg ? rest : p.cg;
+  return ch;
 }
 
-// Iterate the CTA's jobs in wavefront order; f(job) returns false to stop.
-template <class F>
-__device__ __forceinline__ void for_each_job(const Ctx& x, int64_t j, int64_t nc, int C, int64_t cb,
-                                             const Span& sl, F f) {
-  const LaneParams& p = *x.p;
-  const int64_t m = j < nc ? (nc - j + C - 1) / C : 0;  // my chunks
-  for (int64_t s = 0; s < m + 4; ++s) {
-    for (int ph = 0; ph < 5; ++ph) {
-      const int64_t ci = s - ph;
-      if (ci < 0 || ci >= m) continue;
-      const int64_t c = j + ci * C;
-      ChunkGeo ch;
-      ch.id = cb + c;
-      ch.g0 = p.round_g0 + sl.start + c * p.cg;
-      const int64_t rest = sl.len - c * p.cg;
-      ch.len = rest < p.cg ? rest : p.cg;
-      const int nj = njobs(x, ph);
-      for (int t = 0; t < nj; ++t) {
-        Job J;
-        make_job(x, ph, ch, t, J);
-        if (!f(J)) return;
-      }
-    }
-  }
-}
-
-template <int DT>
+template <int DT, bool kLsuStore>
 __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_constant__ LaneParams p) {
   using O = Ops<DT>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  volatile int* abort_s = reinterpret_cast<volatile int*>(empty + kStages);
+  TileDesc* desc = reinterpret_cast<TileDesc*>(empty + kStages);
+  RelRec* rel_rec = reinterpret_cast<RelRec*>(desc + kStages);
+  RelRing* ring = reinterpret_cast<RelRing*>(rel_rec + kRelSlots);
+  volatile int* abort_s = reinterpret_cast<volatile int*>(ring + 1);
 
   const int per_rank = p.k * p.C;
   Ctx x;
@@ -295,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
   const Span sl = rf_split(p.round_len, p.k, l);
   const int64_t nc = n_chunks(sl.len, p.cg);
   const int64_t cb = chunk_base(p.round_len, p.k, l, p.cg);
+  const int64_t m = j < nc ? (nc - j + p.C - 1) / p.C : 0;  // my chunks: j, j+C, ...
 
   const int tid = threadIdx.x;
   if (tid == 0) {
@@ -303,120 +312,323 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       mbar_init(&empty[s], 1);
     }
     *abort_s = 0;
+    ring->tail = 0;
+    ring->head = 0;
+    ring->done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
+  if (tid >= 32 && tid < 64) {
+    // ================================================= releaser (one thread)
+    // Publishes job-completion flags. The fence waits until the job's stores
+    // (issued by every consumer before the storer's barrier, hence
+    // happening-before this thread's acquire of the record) are visible
+    // system-wide; doing it here keeps the consumer pipeline streaming.
+    if (tid != 32) return;
+    const bool tr = p.trace != nullptr;
+    uint64_t tr_fence = 0;
+    int head = 0;
+    for (;;) {
+      const int tail = ring->tail;
+      if (tail == head) {
+        if (ring->done && ring->tail == head) break;
+        continue;
+      }
+      __threadfence_block();  // acquire the record
+      const uint64_t tw = tr ? globaltimer_ns() : 0;
+      __threadfence_system();
+      while (head != tail) {
+        const RelRec& r = rel_rec[head % kRelSlots];
+        for (int i = 0; i < r.n; ++i) st_release_sys(r.f[i], p.epoch);
+        ++head;
+      }
+      ring->head = head;
+      if (tr) tr_fence += globaltimer_ns() - tw;
+    }
+    if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = tr_fence;
+    return;
+  }
+
   if (tid < 32) {
-    // ------------------------------------------------ producer
+    // ================================================= producer (one thread)
+    // Out-of-order issue: among the next job of every phase, take the first
+    // (in phase order A..E) whose flags are already set, subject to
+    //   - per chunk, phase order: job (ph, c) only after every job of the
+    //     previous active phase for chunk c has been issued (local stores of
+    //     an earlier phase must precede the release of a later one);
+    //   - a window: phase A runs at most p_window chunks ahead of the last
+    //     active phase.
+    // Every wait is still on peers' earlier phases of the same chunk, so the
+    // in-order schedule is one possible execution and progress is guaranteed.
     if (tid != 0) return;
+    const bool tr = p.trace != nullptr;
+    uint64_t tr_flag = 0, tr_empty = 0;
+    const uint64_t t_start = tr ? globaltimer_ns() : 0;
+    int nj[5], prev[5], last = -1;
+    int64_t cur[5];
+    int sub[5];
+    for (int ph = 0, pa = -1; ph < 5; ++ph) {
+      nj[ph] = njobs(x, ph);
+      cur[ph] = nj[ph] > 0 ? 0 : m;  // inactive phases are "done"
+      sub[ph] = 0;
+      prev[ph] = pa;
+      if (nj[ph] > 0) pa = last = ph;
+    }
+    const int64_t window = 6;
     int64_t k = 0;  // global tile counter
-    for_each_job(x, j, nc, p.C, cb, sl, [&](const Job& J) {
-      for (int w = 0; w < J.nwait; ++w)
-        if (!wait_one(p, J.wait[w])) {
-          *abort_s = 1;
-          return false;
+    bool ok = true;
+    uint64_t t_idle = 0;
+    while (ok) {
+      int pick = -1;
+      Job J;
+      bool any_left = false;
+      for (int ph = 0; ph < 5 && pick < 0; ++ph) {
+        if (cur[ph] >= m) continue;
+        any_left = true;
+        if (prev[ph] >= 0 && cur[ph] >= cur[prev[ph]]) continue;  // previous phase not issued yet
+        if (ph == 0 && last >= 0 && last != 0 && cur[0] - cur[last] >= window) continue;
+        make_job(x, ph, chunk_geo(p, cb, sl, j + cur[ph] * p.C), sub[ph], J);
+        bool ready = true;
+        for (int w = 0; w < J.nwait && ready; ++w) ready = flag_ready(p, J.wait[w]);
+        if (ready) pick = ph;
+      }
+      if (!any_left) break;
+      if (pick < 0) {  // nothing ready: watchdog + abort checks
+        const uint64_t now = globaltimer_ns();
+        if (t_idle == 0) t_idle = now;
+        if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) ok = false;
+        if (now - t_idle > p.timeout_ns) {
+          atomicExch(p.abort_flag, 1u);
+          *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_TIMEOUT);
+          __threadfence_system();
+          ok = false;
         }
-      if (J.nwait) fence_async_global();  // order the acquire before async-proxy reads
+        continue;
+      }
+      if (t_idle) {
+        if (tr) tr_flag += globaltimer_ns() - t_idle;
+        t_idle = 0;
+      }
+      if (J.nwait) fence_async_global();  // acquire (generic proxy) before async-proxy reads
+      // advance the phase cursor
+      if (++sub[pick] == nj[pick]) {
+        sub[pick] = 0;
+        ++cur[pick];
+      }
       const int64_t T = tile_granules(J.nsrc);
-      const int64_t nt = n_tiles(J);
-      for (int64_t t = 0; t < nt; ++t, ++k) {
+      const int64_t nt = J.len > 0 ? (J.len + T - 1) / T : 1;  // empty jobs keep one empty tile
+      for (int64_t t = 0; t < nt && ok; ++t, ++k) {
         const int s = (int)(k % kStages);
         if (k >= kStages) {
           const uint32_t par = (uint32_t)(((k / kStages) - 1) & 1);
           uint32_t spins = 0;
+          const uint64_t te = tr ? globaltimer_ns() : 0;
           while (!mbar_try_wait(&empty[s], par)) {
             if ((++spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(p.abort_flag)) {
-              *abort_s = 1;
-              return false;
+              ok = false;
+              break;
             }
           }
+          if (tr) tr_empty += globaltimer_ns() - te;
+          if (!ok) break;
         }
         const int64_t g0 = t * T;
         const int64_t tl = J.len - g0 < T ? J.len - g0 : T;  // may be 0 (empty job)
-        const bool part = J.x_src >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
+        const bool xpart = J.x_src >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
+        const bool rpart = J.recv_dst >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
+        const int64_t poff = (xpart || rpart) ? x.msg.partial_g - (J.m0 + g0) : -1;
         uint4* stage = reinterpret_cast<uint4*>(smem + (size_t)s * kStageBytes);
+        TileDesc& d = desc[s];
+        d.nsrc = J.nsrc;
+        d.ndst = J.ndst;
+        d.recv_dst = rpart ? J.recv_dst : -1;
+        d.ph = J.ph;
+        d.T = T;
+        d.tl = tl;
+        d.poff = poff;
+        d.dst[0] = J.dst[0] + g0;
+        d.dst[1] = J.ndst > 1 ? J.dst[1] + g0 : nullptr;
+        d.nrel = (t == nt - 1) ? J.nrel : 0;
+        for (int r = 0; r < d.nrel; ++r) d.rel[r] = J.rel[r];
         uint32_t tx = 0;
         for (int i = 0; i < J.nsrc; ++i) {
           int64_t cnt = tl;
-          if (part && i == J.x_src) {  // the message's partial last granule: generic load
-            const int64_t off = x.msg.partial_g - (J.m0 + g0);
-            stage[i * T + off] = load_partial(J.src[i] + g0 + off, x.msg.partial_bytes);
-            cnt = off;  // the partial granule is the last granule of the message
+          if (xpart && i == J.x_src) {  // partial last granule of sendbuf: generic load
+            stage[i * T + poff] = load_partial(J.src[i] + g0 + poff, x.msg.partial_bytes);
+            cnt = poff;
           }
           if (cnt > 0) tx += (uint32_t)(cnt * 16);
         }
-        if (part) fence_async_smem();
+        fence_async_smem();
         mbar_arrive_tx(&full[s], tx);
         for (int i = 0; i < J.nsrc; ++i) {
-          int64_t cnt = tl;
-          if (part && i == J.x_src) cnt = x.msg.partial_g - (J.m0 + g0);
+          const int64_t cnt = (xpart && i == J.x_src) ? poff : tl;
           if (cnt > 0) bulk_load(stage + i * T, J.src[i] + g0, (uint32_t)(cnt * 16), &full[s]);
         }
       }
-      return true;
-    });
+    }
+    // end marker (also sent after an abort so consumers exit)
+    {
+      const int s = (int)(k % kStages);
+      if (ok && k >= kStages) {
+        const uint32_t par = (uint32_t)(((k / kStages) - 1) & 1);
+        uint32_t spins = 0;
+        while (!mbar_try_wait(&empty[s], par))
+          if ((++spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(p.abort_flag)) break;
+      }
+      desc[s].nsrc = 0;
+      if (!ok) *abort_s = 1;
+      mbar_arrive_tx(&full[s], 0);
+    }
+    if (tr) {
+      uint64_t* Tr = p.trace + (size_t)blockIdx.x * kTraceWords;
+      Tr[kTrProdTotal] = globaltimer_ns() - t_start;
+      Tr[kTrProdFlagWait] = tr_flag;
+      Tr[kTrProdEmptyWait] = tr_empty;
+      Tr[kTrProdTiles] = (uint64_t)k;
+    }
     return;
   }
 
-  // -------------------------------------------------- consumers (+ storer)
-  const int ct = tid - 32;
+  // ================================================ consumers (+ storer)
+  const int ct = tid - 64;
   const bool storer = ct == 0;
-  int64_t k = 0;
-  int64_t freed = -1;  // highest tile index whose stage was returned to the producer
-  for_each_job(x, j, nc, p.C, cb, sl, [&](const Job& J) {
-    const int64_t T = tile_granules(J.nsrc);
-    const int64_t nt = n_tiles(J);
-    for (int64_t t = 0; t < nt; ++t, ++k) {
-      const int s = (int)(k % kStages);
-      const uint32_t par = (uint32_t)((k / kStages) & 1);
-      uint32_t spins = 0;
-      while (!mbar_try_wait(&full[s], par)) {
-        if ((++spins & 1023u) == 0 && *abort_s) return false;
+  const bool tr = storer && p.trace != nullptr;
+  uint64_t tr_full = 0, tr_sync = 0, tr_read = 0, tr_flush = 0, tr_ph[5] = {0, 0, 0, 0, 0}, tr_bytes = 0;
+  uint64_t tr_jobs = 0;
+  const uint64_t t_start = tr ? globaltimer_ns() : 0;
+  int64_t freed = -1;  // bulk mode: highest tile whose stage was returned to the producer
+  for (int64_t k = 0;; ++k) {
+    const int s = (int)(k % kStages);
+    const uint32_t par = (uint32_t)((k / kStages) & 1);
+    uint32_t spins = 0;
+    const uint64_t tf = tr ? globaltimer_ns() : 0;
+    bool aborted = false;
+    while (!mbar_try_wait(&full[s], par)) {
+      if ((++spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(p.abort_flag)) {
+        aborted = true;
+        break;
       }
-      const int64_t g0 = t * T;
-      const int64_t tl = J.len - g0 < T ? J.len - g0 : T;
-      uint4* stage = reinterpret_cast<uint4*>(smem + (size_t)s * kStageBytes);
-      if (J.nsrc > 1) {  // canonical-order reduction, in place into slot 0
+    }
+    if (aborted) break;
+    const uint64_t t_tile = tr ? globaltimer_ns() : 0;
+    if (tr) tr_full += t_tile - tf;
+    const TileDesc& d = desc[s];
+    const int nsrc = d.nsrc;
+    if (nsrc == 0) break;
+    const int64_t T = d.T, tl = d.tl, poff = d.poff;
+    const int ndst = d.ndst, rdst = d.recv_dst, nrel = d.nrel, ph = d.ph;
+    uint4* dst0 = d.dst[0];
+    uint4* dst1 = d.dst[1];
+    uint4* stage = reinterpret_cast<uint4*>(smem + (size_t)s * kStageBytes);
+    if constexpr (kLsuStore) {
+      for (int64_t i = ct; i < tl; i += kConsumers) {
+        uint4 v;
+        if (nsrc > 1) {  // canonical-order reduction in registers
+          typename O::Acc acc;
+          O::init(acc, stage[i]);
+          for (int q = 1; q < nsrc; ++q) O::add(acc, stage[q * T + i]);
+          v = O::narrow(acc);
+        } else {
+          v = stage[i];
+        }
+        if (i == poff && rdst == 0)
+          store_partial(dst0 + i, v, x.msg.partial_bytes);
+        else
+          st_cg(dst0 + i, v);
+        if (ndst > 1) {
+          if (i == poff && rdst == 1)
+            store_partial(dst1 + i, v, x.msg.partial_bytes);
+          else
+            st_cg(dst1 + i, v);
+        }
+      }
+      const uint64_t ts = tr ? globaltimer_ns() : 0;
+      consumers_sync();  // every consumer has read the stage and issued its stores
+      if (tr) tr_sync += globaltimer_ns() - ts;
+      if (storer) {
+        if (nrel > 0) {  // job complete: hand its releases to the releaser warp
+          const uint64_t tw = tr ? globaltimer_ns() : 0;
+          const int tail = ring->tail;
+          while (tail - ring->head >= kRelSlots) {
+          }
+          RelRec& r = rel_rec[tail % kRelSlots];
+          r.n = nrel;
+          for (int i = 0; i < nrel; ++i) r.f[i] = d.rel[i];
+          __threadfence_block();
+          ring->tail = tail + 1;
+          if (tr) tr_flush += globaltimer_ns() - tw;
+        }
+        mbar_arrive(&empty[s]);
+      }
+    } else {
+      if (nsrc > 1) {  // canonical-order reduction, in place into slot 0
         for (int64_t i = ct; i < tl; i += kConsumers) {
           typename O::Acc acc;
           O::init(acc, stage[i]);
-          for (int q = 1; q < J.nsrc; ++q) O::add(acc, stage[q * T + i]);
+          for (int q = 1; q < nsrc; ++q) O::add(acc, stage[q * T + i]);
           stage[i] = O::narrow(acc);
         }
         fence_async_smem();
       }
+      const uint64_t ts = tr ? globaltimer_ns() : 0;
       consumers_sync();
+      if (tr) tr_sync += globaltimer_ns() - ts;
       if (storer) {
-        const bool rpart = J.recv_dst >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
-        for (int d = 0; d < J.ndst; ++d) {
+        uint32_t* rel[kMaxSrc];
+        for (int r = 0; r < nrel; ++r) rel[r] = d.rel[r];
+        for (int dd = 0; dd < ndst; ++dd) {
+          uint4* dp = dd == 0 ? dst0 : dst1;
           int64_t cnt = tl;
-          if (rpart && d == J.recv_dst) {
-            const int64_t off = x.msg.partial_g - (J.m0 + g0);
-            store_partial(J.dst[d] + g0 + off, stage[off], x.msg.partial_bytes);
-            cnt = off;
+          if (poff >= 0 && dd == rdst) {
+            store_partial(dp + poff, stage[poff], x.msg.partial_bytes);
+            cnt = poff;
           }
-          if (cnt > 0) bulk_store(J.dst[d] + g0, stage, (uint32_t)(cnt * 16));
+          if (cnt > 0) bulk_store(dp, stage, (uint32_t)(cnt * 16));
         }
         bulk_commit();
-        bulk_wait_read1();  // all store groups but this tile's have read their smem
-        if (k - 1 > freed && k >= 1) {
+        const uint64_t tq = tr ? globaltimer_ns() : 0;
+        bulk_wait_read1();  // every store group but this tile's has read its smem
+        if (tr) tr_read += globaltimer_ns() - tq;
+        if (k >= 1 && k - 1 > freed) {
           mbar_arrive(&empty[(k - 1) % kStages]);
           freed = k - 1;
         }
-        if (t == nt - 1 && J.nrel > 0) {  // job complete: make it visible, then release
+        if (nrel > 0) {  // job complete: make its stores visible, then release
+          const uint64_t tw = tr ? globaltimer_ns() : 0;
           bulk_wait_all();
+          if (tr) tr_flush += globaltimer_ns() - tw;
           mbar_arrive(&empty[s]);
           freed = k;
           fence_async_global();
           __threadfence_system();
-          for (int r = 0; r < J.nrel; ++r) st_release_sys(J.rel[r], p.epoch);
+          for (int r = 0; r < nrel; ++r) st_release_sys(rel[r], p.epoch);
         }
       }
     }
-    return true;
-  });
-  if (storer) bulk_wait_all();
+    if (tr) {
+      tr_ph[ph] += globaltimer_ns() - t_tile;
+      tr_bytes += (uint64_t)tl * 16 * ndst;
+      if (nrel) ++tr_jobs;
+    }
+  }
+  if (!kLsuStore && storer) bulk_wait_all();
+  if (storer) {
+    __threadfence_block();
+    ring->done = 1;
+  }
+  if (tr) {
+    uint64_t* Tr = p.trace + (size_t)blockIdx.x * kTraceWords;
+    Tr[kTrStoreTotal] = globaltimer_ns() - t_start;
+    Tr[kTrStoreFullWait] = tr_full;
+    Tr[kTrStoreSync] = tr_sync;
+    if (!kLsuStore) Tr[kTrStoreReadWait] = tr_read;
+    Tr[kTrStoreFlush] = tr_flush;
+    Tr[kTrStoreJobs] = tr_jobs;
+    for (int i = 0; i < 5; ++i) Tr[kTrPhaseA + i] = tr_ph[i];
+    Tr[kTrBytes] = tr_bytes;
+  }
 }
 
 }  // namespace tma

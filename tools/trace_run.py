@@ -1,0 +1,81 @@
+"""Per-CTA stall accounting of one lane allreduce launch (LANE_TRACE=1).
+
+torchrun --nproc-per-node P tools/trace_run.py --layout 2x1 [--k 1] [--mib 1024]
+python tools/trace_run.py --emulated --layout 2x4
+Prints, per rank, the mean / max over CTAs of every trace field in microseconds.
+"""
+import argparse
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ["LANE_TRACE"] = "1"
+
+import torch  # noqa: E402
+
+import paper_2508_13397_b200 as lane  # noqa: E402
+from seeded_inputs import device as sdev  # noqa: E402
+
+
+def summarize(tr, label):
+    keys = lane.LaneComm.TRACE_FIELDS
+    out = [label]
+    for key in keys:
+        v = [t[key] for t in tr]
+        if key in ("prod_tiles", "store_jobs", "bytes_stored"):
+            out.append(f"  {key:16s} mean {statistics.mean(v):12.1f}  max {max(v):12.1f}")
+        else:
+            out.append(f"  {key:16s} mean {statistics.mean(v) / 1e3:9.1f} us  max {max(v) / 1e3:9.1f} us")
+    return "\n".join(out)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--layout", default="2x1")
+    ap.add_argument("--k", type=int, default=1)
+    ap.add_argument("--mib", type=float, default=1024)
+    ap.add_argument("--dtype", default="float32")
+    ap.add_argument("--emulated", action="store_true")
+    a = ap.parse_args()
+    N, G = map(int, a.layout.split("x"))
+    tdt = getattr(torch, a.dtype)
+    n = int(a.mib * (1 << 20)) // (2 if a.dtype == "bfloat16" else 4)
+    if a.emulated:
+        emu = lane.LaneEmulator(N, G, a.k, device=0)
+        ins = [sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), a.dtype, "signed", 1, p) for p in range(N * G)]
+        outs = [torch.empty_like(t) for t in ins]
+        for _ in range(3):
+            emu.allreduce(outs, ins)
+        torch.cuda.synchronize()
+        print(summarize(emu.trace(), f"emulated {a.layout} k={a.k}"), flush=True)
+        return
+    import torch.distributed as dist
+    rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    comm = lane.LaneComm(N, G, a.k, rank=rank, device=local)
+    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), a.dtype, "signed", 1, rank)
+    out = torch.empty_like(inp)
+    for _ in range(3):
+        comm.allreduce(out, inp)
+    torch.cuda.synchronize()
+    dist.barrier()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    comm.allreduce(out, inp)
+    e.record()
+    torch.cuda.synchronize()
+    tr = comm.trace()
+    txt = summarize(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e):.3f} ms")
+    for r in range(dist.get_world_size()):
+        if r == rank:
+            print(txt, flush=True)
+        dist.barrier()
+    comm.close()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
