@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--sweep", default=None,
+                    help="multi-GPU: write busbw vs message size (ours and NCCL ring) as JSONL to this file")
     return ap.parse_args()
 
 
@@ -414,8 +416,58 @@ def nccl_ring(inp, S, P, args, dist, stream):
             "algo": os.environ.get("NCCL_ALGO", "default"), "version": ".".join(map(str, torch.cuda.nccl.version()))}
 
 
+def run_sweep(args):
+    """busbw vs message size, 1 MiB .. args.mib per rank, ours vs NCCL ring
+    (BASELINE metric x-axis). One JSON object per size to args.sweep."""
+    import torch
+    import torch.distributed as dist
+    import paper_2508_13397_b200 as lane
+    from seeded_inputs import device as sdev
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("cpu:gloo,cuda:nccl")
+    N, G = layout_for(args, world)
+    P, dtype, isz = world, args.dtype, itemsize(args.dtype)
+    comm = lane.LaneComm(N, G, args.k, rank=rank, device=local)
+    stream = torch.cuda.current_stream()
+    mib = 1
+    rows = []
+    while mib <= args.mib:
+        n = (mib << 20) // isz
+        S = n * isz
+        inp = sdev.fill(torch.empty(n, dtype=getattr(torch, dtype), device="cuda"), dtype, "signed", 42, rank)
+        out = torch.empty_like(inp)
+        steps = max(5, min(200, int(2000 / mib)))
+        ms = device_time_ms(lambda: comm.allreduce(out, inp), steps, 5, stream, lambda: dist.barrier())
+        ok = sample_check([out], N, G, dtype, n, 42, [rank])
+        buf = inp.clone()
+        ms_n = device_time_ms(lambda: dist.all_reduce(buf), steps, 5, stream, lambda: dist.barrier())
+        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        row = {"layout": f"{N}x{G}", "k": args.k, "dtype": dtype, "bytes": S, "ms": round(t[0].item(), 4),
+               "busbw": round(busbw(S, P, t[0].item()), 2), "nccl_ring_ms": round(t[1].item(), 4),
+               "nccl_ring_busbw": round(busbw(S, P, t[1].item()), 2), "verified": t[2].item() == 0,
+               "frac_of_770": round(busbw(S, P, t[0].item()) / NVLINK_PEAK, 4), "plan": comm.plan(n, dtype)}
+        rows.append(row)
+        if rank == 0:
+            print(json.dumps(row), flush=True)
+        del inp, out, buf
+        mib *= 2
+    if rank == 0:
+        with open(args.sweep, "a") as f:
+            for r in rows:
+                f.write(json.dumps(r) + "\n")
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    if args.sweep:
+        return run_sweep(args)
     if args.impl == "reference":
         return run_reference(args)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -67,6 +67,7 @@ struct lane_comm_s {
   int sm_count = 0;
   int64_t round_cap = 0;   // granules of message per round (kernel launch)
   int64_t cg_max = 0, cg_min = 0;
+  int chunks_per_cta = 4;
   int64_t chunk_cap = 0;   // max chunks per round (flag capacity per flag type)
   uint64_t s1_bytes = 0, s2_bytes = 0, r_bytes = 0, flag_bytes = 0, total_bytes = 0;
   std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
@@ -185,6 +186,8 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->round_cap = env_i64("LANE_ROUND_BYTES", (int64_t)1 << 30) / 16;
   c->cg_max = env_i64("LANE_CHUNK_BYTES", 1 << 20) / 16;
   c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 16 << 10) / 16;
+  c->chunks_per_cta = (int)env_i64("LANE_CHUNKS_PER_CTA", 4);
+  if (c->chunks_per_cta < 1) c->chunks_per_cta = 1;
   if (c->round_cap < 1024) return fail(c, LANE_ERR_INVALID_ARG, "LANE_ROUND_BYTES must be >= 16 KiB");
   if (c->cg_min < 16) c->cg_min = 16;
   if (c->cg_max < c->cg_min) c->cg_max = c->cg_min;
@@ -281,9 +284,10 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
     return fail(c, LANE_ERR_INVALID_ARG,
                 "ctas_per_group*procs_per_gpu exceeds the device's co-resident CTA capacity");
   pl->C = C;
-  // chunk size: give every CTA of a group at least one chunk, within bounds
+  // chunk size: give every CTA of a group about chunks_per_cta chunks (so the
+  // phases of successive chunks overlap), within [cg_min, cg_max]
   int64_t slice0 = (pl->round_len0 + c->k - 1) / c->k;
-  int64_t cg = (slice0 + C - 1) / C;
+  int64_t cg = (slice0 + (int64_t)C * c->chunks_per_cta - 1) / ((int64_t)C * c->chunks_per_cta);
   if (cg > c->cg_max) cg = c->cg_max;
   if (cg < c->cg_min) cg = c->cg_min;
   pl->cg = cg;
@@ -539,6 +543,7 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
   p.nlocal = c->P;
+  p.direct = (c->engine == 1 && env_i64("LANE_DIRECT", 1)) ? 1 : 0;
   for (int r = 0; r < c->P; ++r) {
     p.rk[r].send = static_cast<const char*>(sendbufs[r]);
     p.rk[r].recv = static_cast<char*>(recvbufs[r]);

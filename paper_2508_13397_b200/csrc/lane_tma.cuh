@@ -47,7 +47,7 @@ constexpr int kThreads = 32 * (2 + kConsumerWarps);  // producer warp, releaser 
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
 constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 256 + kRelSlots * 136 + 64;
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 64;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -100,15 +100,16 @@ __device__ __forceinline__ void consumers_sync() {
 }
 
 // ------------------------------------------------------------------ jobs
-// ------------------------------------------------------------------ jobs
 struct Job {
-  int ph;                           // 0..4 = phase A..E
-  int nsrc, ndst, x_src, recv_dst;  // x_src / recv_dst: index or -1
+  int ph;                // 0..4 = phase A..E
+  int nsrc, ndst;
+  uint32_t x_mask;       // bit i: src[i] is a sendbuf (partial last granule possible)
+  uint32_t recv_mask;    // bit d: dst[d] is a recvbuf
   int nwait, nrel;
   int64_t len;  // granules
   int64_t m0;   // message granule of the job's first granule
   const uint4* src[kMaxSrc];
-  uint4* dst[2];
+  uint4* dst[kMaxSrc];
   const uint32_t* wait[kMaxSrc];
   uint32_t* rel[kMaxSrc];
 };
@@ -120,62 +121,89 @@ struct Ctx {
   Msg msg;
 };
 
-// Jobs per chunk of each phase. With G == 1 the phase-1 sum of the own lane
-// sub-part is the sendbuf itself, so B only sends the N-1 remote sub-parts and
-// C reads its own term straight from sendbuf.
+// Jobs per chunk of each phase.
+//  staged (default, unregistered buffers): A push, B reduce+push, C reduce,
+//    D pull lane results, E pull node parts — through library scratch.
+//    With G == 1 the own lane term is the sendbuf itself: B only sends the
+//    N-1 remote sub-parts and C reads its own term from sendbuf.
+//  direct (every rank's sendbuf/recvbuf addressable: emulated mode):
+//    B reduces straight from the node's sendbufs, C stores the lane result
+//    into every lane member's recvbuf, D is a zero-byte job that forwards
+//    "part g complete" to the node, E pulls node peers' parts from their
+//    recvbufs. No phase-1 or R staging.
 __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
+  const bool direct = x.p->direct != 0;
   switch (ph) {
-    case 0: return x.G - 1;
+    case 0: return direct ? 0 : x.G - 1;
     case 1: return x.G == 1 ? x.N - 1 : x.N;
     case 2: return x.N > 1 ? 1 : 0;
-    case 3: return x.N - 1;
+    case 3: return direct ? ((x.N > 1 && x.G > 1) ? 1 : 0) : x.N - 1;
     default: return x.G - 1;
   }
 }
+
+__device__ __forceinline__ uint4* send_of(const RankMem& m) {
+  return reinterpret_cast<uint4*>(const_cast<char*>(m.send));
+}
+__device__ __forceinline__ uint4* recv_of(const RankMem& m) { return reinterpret_cast<uint4*>(m.recv); }
 
 // Job t of phase ph (0=A .. 4=E) for chunk ch.
 __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
   const LaneParams& p = *x.p;
   const int a = x.a, g = x.g, N = x.N, G = x.G;
+  const bool direct = p.direct != 0;
   J.ph = ph;
   J.nsrc = 1;
   J.ndst = 1;
-  J.x_src = -1;
-  J.recv_dst = -1;
+  J.x_mask = 0;
+  J.recv_mask = 0;
   J.nwait = 0;
   J.nrel = 0;
   const Span gp = rf_split(ch.len, G, g);
-  if (ph == 0) {  // A: push part gd of my sendbuf into (a,gd)'s S1
+  if (ph == 0) {  // A (staged): push part gd of my sendbuf into (a,gd)'s S1
     const int gd = (g + 1 + t) % G;
     const Span pd = rf_split(ch.len, G, gd);
     const RankMem& dm = p.rk[a * G + gd];
     J.len = pd.len;
     J.m0 = ch.g0 + pd.start;
     J.src[0] = x.msg.send + J.m0;
-    J.x_src = 0;
+    J.x_mask = 1;
     J.dst[0] = s1_slot(p, dm, g < gd ? g : g - 1, ch.id);
     J.rel[J.nrel++] = dm.flags + f1_idx(p, g, ch.id);
-  } else if (ph == 1) {  // B: reduce part g over the node, sub-part b
+  } else if (ph == 1) {  // B: reduce part g over the node (ascending h), sub-part b
     const int b = (a + 1 + t) % N;  // own sub-part last (absent when G == 1)
     const Span up = rf_split(gp.len, N, b);
     J.len = up.len;
     J.m0 = ch.g0 + gp.start + up.start;
     J.nsrc = G;
-    for (int h = 0; h < G; ++h)
-      J.src[h] = (h == g) ? x.msg.send + J.m0 : s1_slot(p, *x.me, h < g ? h : h - 1, ch.id) + up.start;
-    J.x_src = g;
-    if (t == 0)
-      for (int h = 0; h < G; ++h)
-        if (h != g) J.wait[J.nwait++] = x.me->flags + f1_idx(p, h, ch.id);
+    for (int h = 0; h < G; ++h) {
+      if (direct) {
+        J.src[h] = send_of(p.rk[a * G + h]) + J.m0;
+        J.x_mask |= 1u << h;
+      } else {
+        J.src[h] = (h == g) ? x.msg.send + J.m0 : s1_slot(p, *x.me, h < g ? h : h - 1, ch.id) + up.start;
+      }
+    }
+    if (!direct) {
+      J.x_mask = 1u << g;
+      if (t == 0)
+        for (int h = 0; h < G; ++h)
+          if (h != g) J.wait[J.nwait++] = x.me->flags + f1_idx(p, h, ch.id);
+    }
     if (N > 1) {
       const RankMem& dm = p.rk[b * G + g];
       J.dst[0] = s2_slot(p, dm, a, ch.id);
       J.rel[J.nrel++] = dm.flags + f2_idx(p, a, ch.id);
     } else {  // N == 1: the node sum is the final value of part g
-      J.ndst = 2;
-      J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
-      J.dst[1] = x.msg.recv + J.m0;
-      J.recv_dst = 1;
+      if (direct) {
+        J.dst[0] = x.msg.recv + J.m0;
+        J.recv_mask = 1;
+      } else {
+        J.ndst = 2;
+        J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
+        J.dst[1] = x.msg.recv + J.m0;
+        J.recv_mask = 2;
+      }
       for (int h = 0; h < G; ++h)
         if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
     }
@@ -187,19 +215,40 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
     for (int b = 0; b < N; ++b) {
       if (G == 1 && b == a) {
         J.src[b] = x.msg.send + J.m0;  // T1 of a single-GPU node is its sendbuf
-        J.x_src = b;
+        J.x_mask |= 1u << b;
       } else {
         J.src[b] = s2_slot(p, *x.me, b, ch.id);
         J.wait[J.nwait++] = x.me->flags + f2_idx(p, b, ch.id);
       }
     }
-    J.ndst = 2;
-    J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
-    J.dst[1] = x.msg.recv + J.m0;
-    J.recv_dst = 1;
+    if (direct) {  // lane allgather by pushing F into every lane member's recvbuf
+      J.ndst = N;
+      for (int t2 = 0; t2 < N; ++t2) {
+        const int b = (a + t2) % N;  // own first
+        J.dst[t2] = recv_of(p.rk[b * G + g]) + J.m0;
+      }
+      J.recv_mask = (1u << N) - 1;
+    } else {
+      J.ndst = 2;
+      J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
+      J.dst[1] = x.msg.recv + J.m0;
+      J.recv_mask = 2;
+    }
     for (int b = 0; b < N; ++b)
       if (b != a) J.rel[J.nrel++] = p.rk[b * G + g].flags + f3_idx(p, a, ch.id);
-  } else if (ph == 3) {  // D: pull lane member b's sub-part
+  } else if (ph == 3) {
+    if (direct) {  // D (direct): part g of my recvbuf is complete -> tell the node
+      J.len = 0;
+      J.m0 = ch.g0 + gp.start;
+      J.src[0] = x.msg.recv + J.m0;
+      J.dst[0] = x.msg.recv + J.m0;
+      for (int b = 0; b < N; ++b)
+        if (b != a) J.wait[J.nwait++] = x.me->flags + f3_idx(p, b, ch.id);
+      for (int h = 0; h < G; ++h)
+        if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
+      return;
+    }
+    // D (staged): pull lane member b's sub-part
     const int b = (a + 1 + t) % N;
     const Span up = rf_split(gp.len, N, b);
     J.len = up.len;
@@ -210,23 +259,23 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
       J.ndst = 2;
       J.dst[0] = r_slot(p, *x.me, ch.id) + up.start;
       J.dst[1] = x.msg.recv + J.m0;
-      J.recv_dst = 1;
+      J.recv_mask = 2;
       if (t == N - 2)  // R of part g complete (C's and every D's stores precede this)
         for (int h = 0; h < G; ++h)
           if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
     } else {
       J.dst[0] = x.msg.recv + J.m0;
-      J.recv_dst = 0;
+      J.recv_mask = 1;
     }
-  } else {  // E: pull node peer h's part
+  } else {  // E: pull node peer h's part (from its R, or its recvbuf when direct)
     const int h = (g + 1 + t) % G;
     const Span ph_ = rf_split(ch.len, G, h);
     J.len = ph_.len;
     J.m0 = ch.g0 + ph_.start;
-    J.src[0] = r_slot(p, p.rk[a * G + h], ch.id);
+    J.src[0] = direct ? recv_of(p.rk[a * G + h]) + J.m0 : r_slot(p, p.rk[a * G + h], ch.id);
     J.wait[J.nwait++] = x.me->flags + f4_idx(p, h, ch.id);
     J.dst[0] = x.msg.recv + J.m0;
-    J.recv_dst = 0;
+    J.recv_mask = 1;
   }
 }
 
@@ -237,16 +286,18 @@ __device__ __forceinline__ int64_t tile_granules(int nsrc) {
 // Descriptor of one ring stage, written by the producer before it arrives on
 // the stage's "full" barrier; consumers need nothing else.
 struct TileDesc {
-  int nsrc;       // 0 = end of the CTA's work
-  int ndst, recv_dst, nrel, ph;
-  int64_t T;      // slot stride in granules
-  int64_t tl;     // granules in this tile
-  int64_t poff;   // granule offset of the message's partial last granule in the tile, or -1
-  uint4* dst[2];  // already offset to the tile start
+  int nsrc;            // 0 = end of the CTA's work
+  int ndst, nrel, ph;
+  uint32_t recv_mask;  // dsts that are recvbufs, when the tile holds the partial granule
+  int64_t T;           // slot stride in granules
+  int64_t tl;          // granules in this tile
+  int64_t poff;        // granule offset of the message's partial last granule in the tile, or -1
+  uint4* dst[kMaxSrc]; // already offset to the tile start
   uint32_t* rel[kMaxSrc];  // flags to release once this tile (the job's last) is stored
 };
 
-static_assert(sizeof(TileDesc) <= 256, "TileDesc must fit its smem slot");
+constexpr int kDescBytes = 320;
+static_assert(sizeof(TileDesc) <= kDescBytes, "TileDesc must fit its smem slot");
 
 // A job's flag releases, handed from the storer to the releaser warp.
 struct RelRec {
@@ -435,26 +486,26 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
         }
         const int64_t g0 = t * T;
         const int64_t tl = J.len - g0 < T ? J.len - g0 : T;  // may be 0 (empty job)
-        const bool xpart = J.x_src >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
-        const bool rpart = J.recv_dst >= 0 && x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
+        const bool inpart = x.msg.partial_g >= J.m0 + g0 && x.msg.partial_g < J.m0 + g0 + tl;
+        const bool xpart = J.x_mask != 0 && inpart;
+        const bool rpart = J.recv_mask != 0 && inpart;
         const int64_t poff = (xpart || rpart) ? x.msg.partial_g - (J.m0 + g0) : -1;
         uint4* stage = reinterpret_cast<uint4*>(smem + (size_t)s * kStageBytes);
         TileDesc& d = desc[s];
         d.nsrc = J.nsrc;
         d.ndst = J.ndst;
-        d.recv_dst = rpart ? J.recv_dst : -1;
+        d.recv_mask = rpart ? J.recv_mask : 0u;
         d.ph = J.ph;
         d.T = T;
         d.tl = tl;
         d.poff = poff;
-        d.dst[0] = J.dst[0] + g0;
-        d.dst[1] = J.ndst > 1 ? J.dst[1] + g0 : nullptr;
+        for (int dd = 0; dd < J.ndst; ++dd) d.dst[dd] = J.dst[dd] + g0;
         d.nrel = (t == nt - 1) ? J.nrel : 0;
         for (int r = 0; r < d.nrel; ++r) d.rel[r] = J.rel[r];
         uint32_t tx = 0;
         for (int i = 0; i < J.nsrc; ++i) {
           int64_t cnt = tl;
-          if (xpart && i == J.x_src) {  // partial last granule of sendbuf: generic load
+          if (xpart && ((J.x_mask >> i) & 1u)) {  // partial last granule of a sendbuf: generic load
             stage[i * T + poff] = load_partial(J.src[i] + g0 + poff, x.msg.partial_bytes);
             cnt = poff;
           }
@@ -463,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
         fence_async_smem();
         mbar_arrive_tx(&full[s], tx);
         for (int i = 0; i < J.nsrc; ++i) {
-          const int64_t cnt = (xpart && i == J.x_src) ? poff : tl;
+          const int64_t cnt = (xpart && ((J.x_mask >> i) & 1u)) ? poff : tl;
           if (cnt > 0) bulk_load(stage + i * T, J.src[i] + g0, (uint32_t)(cnt * 16), &full[s]);
         }
       }
@@ -518,7 +569,8 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
     const int nsrc = d.nsrc;
     if (nsrc == 0) break;
     const int64_t T = d.T, tl = d.tl, poff = d.poff;
-    const int ndst = d.ndst, rdst = d.recv_dst, nrel = d.nrel, ph = d.ph;
+    const int ndst = d.ndst, nrel = d.nrel, ph = d.ph;
+    const uint32_t rmask = d.recv_mask;
     uint4* dst0 = d.dst[0];
     uint4* dst1 = d.dst[1];
     uint4* stage = reinterpret_cast<uint4*>(smem + (size_t)s * kStageBytes);
@@ -533,15 +585,12 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
         } else {
           v = stage[i];
         }
-        if (i == poff && rdst == 0)
-          store_partial(dst0 + i, v, x.msg.partial_bytes);
-        else
-          st_cg(dst0 + i, v);
-        if (ndst > 1) {
-          if (i == poff && rdst == 1)
-            store_partial(dst1 + i, v, x.msg.partial_bytes);
+        for (int dd = 0; dd < ndst; ++dd) {
+          uint4* dp = dd == 0 ? dst0 : (dd == 1 ? dst1 : d.dst[dd]);
+          if (i == poff && ((rmask >> dd) & 1u))
+            store_partial(dp + i, v, x.msg.partial_bytes);
           else
-            st_cg(dst1 + i, v);
+            st_cg(dp + i, v);
         }
       }
       const uint64_t ts = tr ? globaltimer_ns() : 0;
@@ -579,9 +628,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
         uint32_t* rel[kMaxSrc];
         for (int r = 0; r < nrel; ++r) rel[r] = d.rel[r];
         for (int dd = 0; dd < ndst; ++dd) {
-          uint4* dp = dd == 0 ? dst0 : dst1;
+          uint4* dp = d.dst[dd];
           int64_t cnt = tl;
-          if (poff >= 0 && dd == rdst) {
+          if (poff >= 0 && ((rmask >> dd) & 1u)) {
             store_partial(dp + poff, stage[poff], x.msg.partial_bytes);
             cnt = poff;
           }
