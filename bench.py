@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-register", action="store_true",
+                    help="multi-GPU: do not register the buffers (staged path through library scratch)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--sweep", default=None,
                     help="multi-GPU: write busbw vs message size (ours and NCCL ring) as JSONL to this file")
@@ -338,6 +340,10 @@ def run_multi(args):
     seed = 42
     inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", seed, rank)
     out = torch.empty_like(inp)
+    registered = not args.no_register
+    if registered:  # zero-copy: the paper shares the user buffer via IPC handles (P L330)
+        comm.register(inp)
+        comm.register(out)
     stream = torch.cuda.current_stream()
     barrier = lambda: dist.barrier()  # noqa: E731
     step = lambda: comm.allreduce(out, inp)  # noqa: E731
@@ -364,6 +370,7 @@ def run_multi(args):
         "config": {"workload": f"{N}x{G} virtual nodes on {world} B200 (one process per GPU, IPC peers over "
                                f"NVLink 5), k={k}, {dtype}, {S >> 20} MiB per rank",
                    "layout": f"{N}x{G}", "procs_per_gpu": k, "bytes_per_rank": S, "emulated": False,
+                   "registered_buffers": registered,
                    "l2": "inputs larger than L2 (1 GiB per rank)", "plan": plan},
         "algbw": round(S / (ms_max * 1e-3) / 1e9, 2),
         "verified": ok,
@@ -438,6 +445,9 @@ def run_sweep(args):
         S = n * isz
         inp = sdev.fill(torch.empty(n, dtype=getattr(torch, dtype), device="cuda"), dtype, "signed", 42, rank)
         out = torch.empty_like(inp)
+        regs = []
+        if not args.no_register:
+            regs = [comm.register(inp), comm.register(out)]
         steps = max(5, min(200, int(2000 / mib)))
         ms = device_time_ms(lambda: comm.allreduce(out, inp), steps, 5, stream, lambda: dist.barrier())
         ok = sample_check([out], N, G, dtype, n, 42, [rank])
@@ -449,9 +459,14 @@ def run_sweep(args):
                "busbw": round(busbw(S, P, t[0].item()), 2), "nccl_ring_ms": round(t[1].item(), 4),
                "nccl_ring_busbw": round(busbw(S, P, t[1].item()), 2), "verified": t[2].item() == 0,
                "frac_of_770": round(busbw(S, P, t[0].item()) / NVLINK_PEAK, 4), "plan": comm.plan(n, dtype)}
+        row["registered_buffers"] = bool(regs)
         rows.append(row)
         if rank == 0:
             print(json.dumps(row), flush=True)
+        torch.cuda.synchronize()
+        dist.barrier()
+        for r_ in regs:
+            comm.deregister(r_)
         del inp, out, buf
         mib *= 2
     if rank == 0:

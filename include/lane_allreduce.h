@@ -101,6 +101,25 @@ int lane_allreduce_open_peers(lane_comm_t comm, const void* all_blobs, size_t bl
 int lane_allreduce(lane_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
                    lane_dtype_t dtype, lane_op_t op, void* stream);
 
+/* Zero-copy registration of a user buffer (collective, same order on every
+ * rank). The paper shares the user buffer between processes through IPC
+ * handles (P L330); here every rank maps every peer's registered buffer so
+ * the kernel reads peers' sendbufs and writes peers' recvbufs directly
+ * (no staging through scratch). register_handle writes this rank's blob
+ * (<= LANE_HANDLE_BYTES) for [ptr, ptr+bytes) — ptr must lie in a cudaMalloc
+ * allocation (not a VMM/expandable segment); the caller all-gathers the blobs
+ * in rank order and calls register_open, which returns reg_id. Afterwards
+ * lane_allreduce on sendbuf/recvbuf inside registered buffers runs zero-copy,
+ * provided every rank passes the same offsets into its registered buffers
+ * (MPI-style symmetric buffers). The registration is owned by the comm until
+ * deregister/finalize; errors: INVALID_ARG, MISALIGNED, CUDA. */
+int lane_allreduce_register_handle(lane_comm_t comm, void* ptr, size_t bytes, void* blob,
+                                   size_t* blob_bytes);
+int lane_allreduce_register_open(lane_comm_t comm, const void* all_blobs, size_t blob_bytes,
+                                 int* reg_id);
+/* Stop using a registration (local; mappings are released at finalize). */
+int lane_allreduce_deregister(lane_comm_t comm, int reg_id);
+
 /* End-to-end variant on HOST buffers: copies host_send to a library-owned
  * device staging buffer, runs lane_allreduce, copies the result to host_recv,
  * all on stream (pinned host memory gives async copies). The caller

@@ -165,6 +165,27 @@ class LaneComm(_CommBase):
         _lib.check(code, self._comm)
         return out
 
+    def register(self, t, group=None) -> int:
+        """Collective: register CUDA tensor ``t`` for zero-copy allreduce (every
+        rank registers its own buffer of the same size, in the same order).
+        Allreduces on tensors inside registered buffers then read peers'
+        sendbufs and write peers' recvbufs directly (P L330 IPC sharing)."""
+        _check_dev_tensor(t, self.device, "t")
+        lib = _lib.load()
+        blob = ctypes.create_string_buffer(HANDLE_BYTES)
+        size = ctypes.c_size_t()
+        nbytes = t.numel() * t.element_size()
+        _lib.check(lib.lane_allreduce_register_handle(self._comm, t.data_ptr(), nbytes, blob, ctypes.byref(size)),
+                   self._comm)
+        blobs = exchange_blobs(bytes(blob.raw[:size.value]), group)
+        rid = ctypes.c_int()
+        _lib.check(lib.lane_allreduce_register_open(self._comm, b"".join(blobs), size.value, ctypes.byref(rid)),
+                   self._comm)
+        return rid.value
+
+    def deregister(self, reg_id: int) -> None:
+        _lib.check(_lib.load().lane_allreduce_deregister(self._comm, reg_id), self._comm)
+
     def allreduce_host(self, out_host, inp_host, stream=None):
         """End-to-end allreduce of HOST tensors (H2D, kernels, D2H on one
         stream). Synchronizes the stream before returning."""

@@ -54,6 +54,9 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_emulated": (I, [P, PP, PP, SZ, I, I, P]),
         "lane_allreduce_emulated_host": (I, [P, PP, PP, SZ, I, I, P]),
         "lane_allreduce_finalize": (I, [P]),
+        "lane_allreduce_register_handle": (I, [P, P, SZ, P, ctypes.POINTER(SZ)]),
+        "lane_allreduce_register_open": (I, [P, P, SZ, ctypes.POINTER(I)]),
+        "lane_allreduce_deregister": (I, [P, I]),
         "lane_allreduce_last_error": (ctypes.c_char_p, [P]),
         "lane_allreduce_check": (I, [P]),
         "lane_allreduce_trace": (I, [P, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)]),

@@ -81,6 +81,17 @@ struct lane_comm_s {
   uint64_t timeout_ns = 0;
   uint64_t* trace = nullptr;  // LANE_TRACE=1: kTraceWords per CTA of the last launch
   int trace_ctas = 0;
+  struct Reg {             // a registered user buffer and its peers' mappings
+    char* base;
+    uint64_t bytes;
+    char* peer[LANE_MAX_RANKS];
+    bool live;
+  };
+  std::vector<Reg> regs;
+  char* pending_reg = nullptr;  // set by register_handle, consumed by register_open
+  uint64_t pending_bytes = 0;
+  std::vector<std::pair<std::string, void*>> ipc_cache;  // opened peer allocations by handle
+  int64_t ctl = 0;             // flag index of the control words
   std::vector<char*> stage;  // device staging for the host-buffer API
   uint64_t stage_bytes = 0;
   std::string last_error;
@@ -129,7 +140,8 @@ void size_scratch(lane_comm_t c) {
   c->s1_bytes = (uint64_t)((G - 1) * slot_g) * 16;
   c->s2_bytes = (uint64_t)(N * slot_u) * 16;
   c->r_bytes = (uint64_t)slot_g * 16;
-  c->flag_bytes = (uint64_t)((2 * G + 2 * N) * c->chunk_cap) * 4;
+  c->ctl = (2 * G + 2 * N) * c->chunk_cap;  // enter[P], done[P], counter follow the chunk flags
+  c->flag_bytes = (uint64_t)(c->ctl + 2 * LANE_MAX_RANKS + 1) * 4;
   auto al = [](uint64_t x) { return (x + 4095) & ~(uint64_t)4095; };
   c->s1_bytes = al(c->s1_bytes);
   c->s2_bytes = al(c->s2_bytes);
@@ -313,6 +325,7 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.err = c->err_dev;
   p.abort_flag = c->abort_dev;
   p.trace = c->trace;
+  p.ctl = c->ctl;
   return p;
 }
 
@@ -387,6 +400,43 @@ int copy_p1(lane_comm_t c, const void* s, void* r, const Plan& pl, cudaStream_t 
   if (e != cudaSuccess) return cuda_fail(c, e, "lane_copy_kernel launch");
   return LANE_OK;
 }
+
+int find_reg(lane_comm_t c, const void* ptr, uint64_t bytes) {
+  const char* q = static_cast<const char*>(ptr);
+  for (size_t i = 0; i < c->regs.size(); ++i) {
+    const auto& r = c->regs[i];
+    if (r.live && q >= r.base && q + bytes <= r.base + r.bytes) return (int)i;
+  }
+  return -1;
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no -lcuda,
+// so the library still loads on hosts without a driver).
+typedef int (*GetRangeFn)(unsigned long long*, size_t*, unsigned long long);
+
+int alloc_base(lane_comm_t c, const void* ptr, char** base) {
+  static GetRangeFn fn = nullptr;
+  if (!fn) {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !f) return cuda_fail(c, e, "cudaGetDriverEntryPoint(cuMemGetAddressRange)");
+    fn = reinterpret_cast<GetRangeFn>(f);
+  }
+  unsigned long long b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (unsigned long long)(uintptr_t)ptr) != 0)
+    return fail(c, LANE_ERR_INVALID_ARG, "register: ptr is not device memory from cudaMalloc");
+  *base = reinterpret_cast<char*>((uintptr_t)b);
+  return LANE_OK;
+}
+
+struct RegBlob {
+  uint32_t magic;
+  int32_t rank;
+  uint64_t bytes, offset;
+  cudaIpcMemHandle_t handle;
+};
 
 int ensure_stage(lane_comm_t c, uint64_t bytes) {
   const int nbuf = 2 * (c->emulated ? c->P : 1);
@@ -519,6 +569,22 @@ int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t cou
   p.nlocal = 1;
   p.rk[c->rank].send = static_cast<const char*>(sendbuf);
   p.rk[c->rank].recv = static_cast<char*>(recvbuf);
+  // zero-copy when both buffers are registered (P L330: the user buffer is
+  // shared through IPC handles); peers use the same offsets into theirs
+  const int rs = find_reg(c, sendbuf, bytes), rr = find_reg(c, recvbuf, bytes);
+  if (c->engine == 1 && rs >= 0 && rr >= 0 && env_i64("LANE_DIRECT", 2)) {
+    const auto& S = c->regs[rs];
+    const auto& R = c->regs[rr];
+    const uint64_t so = (uint64_t)(static_cast<const char*>(sendbuf) - S.base);
+    const uint64_t ro = (uint64_t)(static_cast<char*>(recvbuf) - R.base);
+    for (int q = 0; q < c->P; ++q)
+      if (q != c->rank) {
+        p.rk[q].send = S.peer[q] + so;
+        p.rk[q].recv = R.peer[q] + ro;
+      }
+    p.direct = env_i64("LANE_DIRECT", 2) == 1 ? 1 : 2;  // push flavour by default on real peers
+    p.handshake = 1;
+  }
   return launch_rounds(c, p, pl, dtype, s);
 }
 
@@ -598,6 +664,74 @@ int lane_allreduce_emulated_host(lane_comm_t c, const void* const* host_sends,
   return LANE_OK;
 }
 
+int lane_allreduce_register_handle(lane_comm_t c, void* ptr, size_t bytes, void* blob,
+                                   size_t* blob_bytes) {
+  if (!c || !ptr || !blob || !blob_bytes) return fail(c, LANE_ERR_INVALID_ARG, "register: null argument");
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "register: emulated comms address every buffer already");
+  if ((uintptr_t)ptr & 15) return fail(c, LANE_ERR_MISALIGNED, "register: ptr must be 16-byte aligned");
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  char* base = nullptr;
+  int st = alloc_base(c, ptr, &base);
+  if (st != LANE_OK) return st;
+  RegBlob b;
+  memset(&b, 0, sizeof(b));
+  b.magic = kMagic ^ 0x52454721u;
+  b.rank = c->rank;
+  b.bytes = bytes;
+  b.offset = (uint64_t)(static_cast<char*>(ptr) - base);
+  LANE_CUDA(c, cudaIpcGetMemHandle(&b.handle, base));
+  memcpy(blob, &b, sizeof(b));
+  *blob_bytes = sizeof(b);
+  c->pending_reg = static_cast<char*>(ptr);
+  c->pending_bytes = bytes;
+  return LANE_OK;
+}
+
+int lane_allreduce_register_open(lane_comm_t c, const void* all_blobs, size_t blob_bytes, int* reg_id) {
+  if (!c || !all_blobs || !reg_id) return fail(c, LANE_ERR_INVALID_ARG, "register_open: null argument");
+  if (!c->pending_reg) return fail(c, LANE_ERR_INVALID_ARG, "register_open: no register_handle pending");
+  if (blob_bytes < sizeof(RegBlob)) return fail(c, LANE_ERR_INVALID_ARG, "blob_bytes: too small");
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  lane_comm_s::Reg r;
+  memset(&r, 0, sizeof(r));
+  r.base = c->pending_reg;
+  r.bytes = c->pending_bytes;
+  r.live = true;
+  const char* blobs = static_cast<const char*>(all_blobs);
+  for (int q = 0; q < c->P; ++q) {
+    RegBlob b;
+    memcpy(&b, blobs + (size_t)q * blob_bytes, sizeof(b));
+    if (b.magic != (kMagic ^ 0x52454721u) || b.rank != q)
+      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: not register blobs in rank order");
+    if (b.bytes != r.bytes)
+      return fail(c, LANE_ERR_INVALID_ARG, "register: ranks registered buffers of different sizes");
+    if (q == c->rank) {
+      r.peer[q] = r.base;
+      continue;
+    }
+    std::string key(reinterpret_cast<const char*>(&b.handle), sizeof(b.handle));
+    void* mapped = nullptr;
+    for (auto& e : c->ipc_cache)
+      if (e.first == key) mapped = e.second;
+    if (!mapped) {
+      cudaError_t e = cudaIpcOpenMemHandle(&mapped, b.handle, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess) return cuda_fail(c, e, "cudaIpcOpenMemHandle (register)");
+      c->ipc_cache.emplace_back(key, mapped);
+    }
+    r.peer[q] = static_cast<char*>(mapped) + b.offset;
+  }
+  c->pending_reg = nullptr;
+  c->regs.push_back(r);
+  *reg_id = (int)c->regs.size() - 1;
+  return LANE_OK;
+}
+
+int lane_allreduce_deregister(lane_comm_t c, int reg_id) {
+  if (!c || reg_id < 0 || reg_id >= (int)c->regs.size()) return fail(c, LANE_ERR_INVALID_ARG, "reg_id: unknown");
+  c->regs[reg_id].live = false;
+  return LANE_OK;
+}
+
 int lane_allreduce_finalize(lane_comm_t c) {
   if (!c) return LANE_ERR_INVALID_ARG;
   release(c);
@@ -611,6 +745,7 @@ void release(lane_comm_t c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (auto& e : c->ipc_cache) cudaIpcCloseMemHandle(e.second);
   for (char* p : c->own) cudaFree(p);
   for (char* p : c->stage) cudaFree(p);
   if (c->abort_dev) cudaFree(c->abort_dev);

@@ -83,7 +83,9 @@ struct LaneParams {
   int64_t sg, su;       // slot strides (granules): max group part / sub-part
   int64_t cap;          // chunk capacity (flag and slot stride in chunks)
   uint32_t epoch;       // monotonically increasing per round, never reset
-  int direct;           // 1: every rank's send/recv addressable (emulated): zero-copy jobs
+  int direct;           // 1: every rank's send/recv addressable: zero-copy jobs
+  int handshake;        // 1: start/end handshake (registered user buffers on real peers)
+  int64_t ctl;          // flag index of the control words: enter[P], done[P], CTA counter
   uint64_t timeout_ns;
   uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
   uint32_t* abort_flag; // device word: set when any wait of this comm timed out

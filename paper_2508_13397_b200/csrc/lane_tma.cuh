@@ -131,14 +131,20 @@ struct Ctx {
 //    into every lane member's recvbuf, D is a zero-byte job that forwards
 //    "part g complete" to the node, E pulls node peers' parts from their
 //    recvbufs. No phase-1 or R staging.
+//  direct-push (registered user buffers on real peers; all NVLink traffic is
+//    stores, the faster direction on this fabric): A and B as staged, C stores
+//    the lane result into every lane member's recvbuf, D pushes my completed
+//    part g from my recvbuf into the node peers' recvbufs; no pull phase.
+enum DirectMode { kStaged = 0, kDirectPull = 1, kDirectPush = 2 };
+
 __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
-  const bool direct = x.p->direct != 0;
+  const int dm = x.p->direct;
   switch (ph) {
-    case 0: return direct ? 0 : x.G - 1;
+    case 0: return dm == kDirectPull ? 0 : x.G - 1;
     case 1: return x.G == 1 ? x.N - 1 : x.N;
     case 2: return x.N > 1 ? 1 : 0;
-    case 3: return direct ? ((x.N > 1 && x.G > 1) ? 1 : 0) : x.N - 1;
-    default: return x.G - 1;
+    case 3: return dm != kStaged ? ((x.N > 1 && x.G > 1) ? 1 : 0) : x.N - 1;
+    default: return dm == kDirectPush ? 0 : x.G - 1;
   }
 }
 
@@ -151,7 +157,8 @@ __device__ __forceinline__ uint4* recv_of(const RankMem& m) { return reinterpret
 __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
   const LaneParams& p = *x.p;
   const int a = x.a, g = x.g, N = x.N, G = x.G;
-  const bool direct = p.direct != 0;
+  const bool direct = p.direct == kDirectPull;  // pull flavour (emulated mode)
+  const bool push = p.direct == kDirectPush;
   J.ph = ph;
   J.nsrc = 1;
   J.ndst = 1;
@@ -195,6 +202,12 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
       J.dst[0] = s2_slot(p, dm, a, ch.id);
       J.rel[J.nrel++] = dm.flags + f2_idx(p, a, ch.id);
     } else {  // N == 1: the node sum is the final value of part g
+      if (push) {  // phase 3 by pushing part g into every node member's recvbuf
+        J.ndst = G;
+        for (int t2 = 0; t2 < G; ++t2) J.dst[t2] = recv_of(p.rk[a * G + (g + t2) % G]) + J.m0;
+        J.recv_mask = (1u << G) - 1;
+        return;  // completion is covered by the end-of-call handshake
+      }
       if (direct) {
         J.dst[0] = x.msg.recv + J.m0;
         J.recv_mask = 1;
@@ -221,7 +234,7 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
         J.wait[J.nwait++] = x.me->flags + f2_idx(p, b, ch.id);
       }
     }
-    if (direct) {  // lane allgather by pushing F into every lane member's recvbuf
+    if (direct || push) {  // lane allgather by pushing F into every lane member's recvbuf
       J.ndst = N;
       for (int t2 = 0; t2 < N; ++t2) {
         const int b = (a + t2) % N;  // own first
@@ -235,8 +248,19 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
       J.recv_mask = 2;
     }
     for (int b = 0; b < N; ++b)
-      if (b != a) J.rel[J.nrel++] = p.rk[b * G + g].flags + f3_idx(p, a, ch.id);
+      if (b != a || push) J.rel[J.nrel++] = p.rk[b * G + g].flags + f3_idx(p, a, ch.id);
   } else if (ph == 3) {
+    if (push) {  // D (push): part g of my recvbuf is complete -> store it into the node's recvbufs
+      J.len = gp.len;
+      J.m0 = ch.g0 + gp.start;
+      J.src[0] = x.msg.recv + J.m0;
+      J.x_mask = 1;  // a user buffer: its partial last granule is loaded generically
+      for (int b = 0; b < N; ++b) J.wait[J.nwait++] = x.me->flags + f3_idx(p, b, ch.id);
+      J.ndst = G - 1;
+      for (int t2 = 1; t2 < G; ++t2) J.dst[t2 - 1] = recv_of(p.rk[a * G + (g + t2) % G]) + J.m0;
+      J.recv_mask = (1u << (G - 1)) - 1;
+      return;
+    }
     if (direct) {  // D (direct): part g of my recvbuf is complete -> tell the node
       J.len = 0;
       J.m0 = ch.g0 + gp.start;
@@ -314,6 +338,24 @@ struct RelRing {
 
 __device__ __forceinline__ bool flag_ready(const LaneParams& p, const uint32_t* f) {
   return (int32_t)(ld_acquire_sys(f) - p.epoch) >= 0;
+}
+
+// Blocking acquire-wait on one flag (single thread). false on timeout / abort.
+__device__ bool wait_one(const LaneParams& p, const uint32_t* f) {
+  if (flag_ready(p, f)) return true;
+  const uint64_t t0 = globaltimer_ns();
+  for (uint32_t it = 1;; ++it) {
+    if (flag_ready(p, f)) return true;
+    if ((it & 63u) == 0) {
+      if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) return false;
+      if (globaltimer_ns() - t0 > p.timeout_ns) {
+        atomicExch(p.abort_flag, 1u);
+        *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_TIMEOUT);
+        __threadfence_system();
+        return false;
+      }
+    }
+  }
 }
 
 __device__ __forceinline__ ChunkGeo chunk_geo(const LaneParams& p, int64_t cb, const Span& sl, int64_t c) {
@@ -397,7 +439,24 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       ring->head = head;
       if (tr) tr_fence += globaltimer_ns() - tw;
     }
+    __threadfence_system();  // every store this CTA made is visible system-wide
     if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = tr_fence;
+    if (p.handshake) {
+      // end of call (registered user buffers): the last CTA of this rank tells
+      // every peer "done with your buffers" and waits until every peer is done
+      // with ours, so the call completes only when no peer still reads our
+      // sendbuf or writes our recvbuf.
+      uint32_t* cnt = x.me->flags + p.ctl + 2 * p.P;
+      uint32_t old;
+      asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
+      if ((int)old + 1 == per_rank) {
+        atomicExch(cnt, 0u);
+        for (int q = 0; q < p.P; ++q)
+          if (q != x.rank) st_release_sys(p.rk[q].flags + p.ctl + p.P + x.rank, p.epoch);
+        for (int q = 0; q < p.P; ++q)
+          if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + p.P + q)) break;
+      }
+    }
     return;
   }
 
@@ -429,6 +488,16 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
     const int64_t window = 6;
     int64_t k = 0;  // global tile counter
     bool ok = true;
+    if (p.handshake) {
+      // start of call (registered user buffers): a peer's sendbuf is final and
+      // its recvbuf free once its kernel has started (stream order)
+      if (blockIdx.x % per_rank == 0)
+        for (int q = 0; q < p.P; ++q)
+          if (q != x.rank) st_release_sys(p.rk[q].flags + p.ctl + x.rank, p.epoch);
+      for (int q = 0; q < p.P && ok; ++q)
+        if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + q)) ok = false;
+      if (ok) fence_async_global();
+    }
     uint64_t t_idle = 0;
     while (ok) {
       int pick = -1;

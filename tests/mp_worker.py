@@ -47,16 +47,30 @@ def main():
     ks = [1, 4] if args.quick else [1, 2, 4, 8]
     failures = 0
     t0 = time.time()
+    maxb = max(counts) * 4
     for N, G in layouts(P):
         for k in ks:
             comm = lane.LaneComm(N, G, k, rank=rank, device=local)
+            # registered (zero-copy) buffers: one pair per comm, views at offset 0
+            rin = torch.empty(maxb, dtype=torch.uint8, device="cuda")
+            rout = torch.empty(maxb, dtype=torch.uint8, device="cuda")
+            comm.register(rin)
+            comm.register(rout)
             for dtype in ("int32", "float32", "bfloat16"):
                 tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
-                for it, n in enumerate(counts):
-                    seed = 1000 + 17 * n + k
-                    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", seed, rank)
+                isz = torch.empty(0, dtype=tdt).element_size()
+                for it, n in enumerate(counts * 2):
+                    registered = it >= len(counts)
+                    seed = 1000 + 17 * n + k + (7 if registered else 0)
+                    if registered:
+                        inp = sdev.fill(rin[:n * isz].view(tdt), dtype, "signed", seed, rank)
+                    else:
+                        inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", seed, rank)
                     inplace = it % 2 == 1
-                    out = inp if inplace else torch.empty_like(inp)
+                    if inplace:
+                        out = inp
+                    else:
+                        out = rout[:n * isz].view(tdt) if registered else torch.empty_like(inp)
                     comm.allreduce(out, inp)
                     torch.cuda.synchronize()
                     comm.check()
@@ -69,7 +83,7 @@ def main():
                     got = to_numpy(out[torch.from_numpy(idx).cuda()], dtype)
                     if not np.array_equal(bits(got), bits(ref)):
                         bad = np.nonzero(bits(got) != bits(ref))[0]
-                        print(f"rank {rank} FAIL {N}x{G} k={k} {dtype} n={n} inplace={inplace}: "
+                        print(f"rank {rank} FAIL {N}x{G} k={k} {dtype} n={n} inplace={inplace} reg={registered}: "
                               f"{len(bad)} mismatches first {idx[bad[:5]]}", flush=True)
                         failures += 1
             dist.barrier()
