@@ -151,6 +151,44 @@ def peaks():
         return {}
 
 
+def method_hbm_bytes(N, G, S):
+    """Compulsory HBM bytes per rank of the three-phase method when every rank's
+    buffers share one HBM (emulated mode; SURVEY §8(d) "HBM: >= 3.1 d, pull
+    design"): read the inputs (S), materialise and re-read the phase-1 result T1
+    (S/G each way), write the lane result into the lane members' recvbufs (S/G),
+    and the phase-3 allgather re-reads and writes the node's other parts
+    ((G-1)/G S each way): S (3 + 1/G). With G = 1 there is no phase 1 or 3 and
+    the floor is the allreduce's own 2 S."""
+    return 2 * S if G == 1 else int(S * (3 + 1 / G))
+
+
+def ncu_traffic(layout, k, dtype, S, P):
+    """DRAM bytes per launch from the committed ncu summary of this workload
+    (profiles/*ncu*summary.json); scaled linearly from the captured size when
+    the captured message size differs. None if there is no capture."""
+    import glob
+    best = None
+    for f in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu*summary.json"))):
+        try:
+            d = json.load(open(f))
+        except (OSError, ValueError):
+            continue
+        w = d.get("workload", "")
+        names = {dtype, SHORT[dtype], "fp32" if dtype == "float32" else dtype}
+        if not (w.startswith(layout + " ") and f"k={k}" in w and any(nm in w for nm in names)):
+            continue
+        kern = [x for x in d.get("kernels", []) if "lane_tma" in x.get("kernel", "")]
+        if not kern or "dram_bytes_per_rank_per_byte" not in kern[0]:
+            continue
+        cand = (abs(d["bytes_per_rank"] - S), f, kern[0]["dram_bytes_per_rank_per_byte"], d["bytes_per_rank"])
+        best = cand if best is None or cand < best else best
+    if best is None:
+        return None, None
+    _, f, per, captured = best
+    note = os.path.basename(f) + ("" if captured == S else f" (scaled from {captured >> 20} MiB/rank)")
+    return int(per * S * P), note
+
+
 def cpu_baseline(N, G, k, dtype, seconds):
     """The oracle as it stands, on this host, single-threaded numpy, on a
     bounded sample of the workload (same layout/dtype, 2^20 elements per rank)."""
@@ -268,13 +306,15 @@ def run_single(args):
         ms = device_time_ms(step, args.steps, args.warmup, stream)
     emu.check()
     ok = sample_check(outs, N, G, dtype, n, seed, range(P))
-    # roofline: HBM. Algorithmic bytes per launch = every rank's input read
-    # once + output written once (2*P*S), the compulsory traffic of an
-    # allreduce whose P buffers share one HBM.
+    # roofline: HBM. Algorithmic bytes per launch = the method's compulsory
+    # HBM traffic with all P ranks in one HBM (method_hbm_bytes);
+    # the plain allreduce floor 2*P*S is reported beside it.
     pk = peaks()
     hbm_peak = float(pk.get("hbm_gbs", 6650.0))
     launches = max(plan["launches"], 1)
-    achieved = 2 * P * S / (ms / launches * 1e-3) / 1e9
+    algo = P * method_hbm_bytes(N, G, S)
+    achieved = algo / launches / (ms / launches * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic(f"{N}x{G}", k, dtype, S, P)
     line = base_line(args, 1, args.steps, args.warmup)
     bw = busbw(S, P, ms)
     line.update({
@@ -288,9 +328,15 @@ def run_single(args):
         "algbw": round(S / (ms * 1e-3) / 1e9, 2),
         "verified": ok,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                     "frac": round(achieved / hbm_peak, 4), "traffic": None,
-                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in pk else "fallback guide",
-                     "algorithmic_bytes_per_launch": 2 * P * S},
+                     "frac": round(achieved / hbm_peak, 4),
+                     "traffic": None if traffic is None else traffic // launches,
+                     "traffic_source": traffic_src,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (measured copy)" if "hbm_gbs" in pk
+                     else "fallback guide",
+                     "algorithmic_bytes_per_launch": algo // launches,
+                     "algorithmic_basis": "method compulsory HBM bytes, P ranks in one HBM: S(3+1/G) per rank",
+                     "allreduce_floor_bytes_per_launch": 2 * P * S // launches,
+                     "frac_of_allreduce_floor": round(2 * P * S / (ms * 1e-3) / 1e9 / hbm_peak, 4)},
         "gpu_launches": args.steps * launches,
         "clocks": clk.summary(),
     })

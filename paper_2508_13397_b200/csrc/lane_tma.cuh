@@ -141,7 +141,7 @@ __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
   const int dm = x.p->direct;
   switch (ph) {
     case 0: return dm == kDirectPull ? 0 : x.G - 1;
-    case 1: return x.G == 1 ? x.N - 1 : x.N;
+    case 1: return x.G == 1 ? (dm == kDirectPull ? 0 : x.N - 1) : x.N;
     case 2: return x.N > 1 ? 1 : 0;
     case 3: return dm != kStaged ? ((x.N > 1 && x.G > 1) ? 1 : 0) : x.N - 1;
     default: return dm == kDirectPush ? 0 : x.G - 1;
@@ -226,8 +226,9 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
     J.m0 = ch.g0 + gp.start + up.start;
     J.nsrc = N;
     for (int b = 0; b < N; ++b) {
-      if (G == 1 && b == a) {
-        J.src[b] = x.msg.send + J.m0;  // T1 of a single-GPU node is its sendbuf
+      if (G == 1 && (b == a || direct)) {
+        // T1 of a single-GPU node is its sendbuf (direct: read the lane member's sendbuf)
+        J.src[b] = (b == a) ? x.msg.send + J.m0 : send_of(p.rk[b * G + g]) + J.m0;
         J.x_mask |= 1u << b;
       } else {
         J.src[b] = s2_slot(p, *x.me, b, ch.id);
