@@ -93,6 +93,9 @@ struct lane_comm_s {
   std::vector<std::pair<std::string, void*>> ipc_cache;  // opened peer allocations by handle
   int64_t ctl = 0;             // flag index of the control words
   std::vector<char*> stage;  // device staging for the host-buffer API
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host API
+  cudaEvent_t ev_start = nullptr, ev_h[2] = {nullptr, nullptr}, ev_k[2] = {nullptr, nullptr},
+              ev_d[2] = {nullptr, nullptr};
   uint64_t stage_bytes = 0;
   std::string last_error;
 };
@@ -439,9 +442,19 @@ struct RegBlob {
 };
 
 int ensure_stage(lane_comm_t c, uint64_t bytes) {
-  const int nbuf = 2 * (c->emulated ? c->P : 1);
+  const int nbuf = 4 * (c->emulated ? c->P : 1);  // 2 pipeline slots x (send, recv) per rank
   if (c->stage_bytes >= bytes && (int)c->stage.size() == nbuf) return LANE_OK;
   for (char* p : c->stage) cudaFree(p);
+  if (c->h2d) {
+    cudaStreamDestroy(c->h2d);
+    cudaStreamDestroy(c->d2h);
+    cudaEventDestroy(c->ev_start);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(c->ev_h[i]);
+      cudaEventDestroy(c->ev_k[i]);
+      cudaEventDestroy(c->ev_d[i]);
+    }
+  }
   c->stage.clear();
   c->stage_bytes = 0;
   for (int i = 0; i < nbuf; ++i) {
@@ -617,6 +630,69 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   return launch_rounds(c, p, pl, dtype, s);
 }
 
+// Pipelined host-buffer allreduce: the message is cut into granule-aligned
+// pieces (each its own collective allreduce — results do not depend on the
+// partition); piece i+1's H2D copy and piece i-1's D2H copy run on library
+// streams while piece i's kernel runs on the caller's stream. Staging is
+// double-buffered; the caller's stream finally waits for the last D2H.
+static int host_pipeline(lane_comm_t c, const void* const* hs, void* const* hr, size_t count, int dtype, int op,
+                  cudaStream_t s) {
+  const int nr = c->emulated ? c->P : 1;
+  const int isz = itemsize_of(dtype);
+  const int q = 16 / isz;
+  int64_t piece = env_i64("LANE_HOST_PIECE_BYTES", 64 << 20) / isz;
+  piece = piece / q * q;
+  if (piece < q) piece = q;
+  if ((uint64_t)piece > count) piece = (int64_t)count;
+  int st = ensure_stage(c, (uint64_t)piece * isz);
+  if (st != LANE_OK) return st;
+  LANE_CUDA(c, cudaSetDevice(c->device));
+  if (!c->h2d) {
+    LANE_CUDA(c, cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    LANE_CUDA(c, cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    LANE_CUDA(c, cudaEventCreateWithFlags(&c->ev_start, cudaEventDisableTiming));
+    for (int i = 0; i < 2; ++i) {
+      LANE_CUDA(c, cudaEventCreateWithFlags(&c->ev_h[i], cudaEventDisableTiming));
+      LANE_CUDA(c, cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+      LANE_CUDA(c, cudaEventCreateWithFlags(&c->ev_d[i], cudaEventDisableTiming));
+    }
+  }
+  // staging reuse across calls is ordered through the caller's stream
+  LANE_CUDA(c, cudaEventRecord(c->ev_start, s));
+  LANE_CUDA(c, cudaStreamWaitEvent(c->h2d, c->ev_start, 0));
+  std::vector<const void*> sends(nr);
+  std::vector<void*> recvs(nr);
+  const int64_t np = ((int64_t)count + piece - 1) / piece;
+  for (int64_t i = 0; i < np; ++i) {
+    const int slot = (int)(i & 1);
+    const uint64_t off = (uint64_t)i * piece;
+    const uint64_t n = ((uint64_t)piece < count - off) ? (uint64_t)piece : count - off;
+    if (i >= 2) LANE_CUDA(c, cudaStreamWaitEvent(c->h2d, c->ev_k[slot], 0));  // kernel i-2 read its send slot
+    for (int r = 0; r < nr; ++r) {
+      char* ss = c->stage[4 * r + 2 * slot];
+      LANE_CUDA(c, cudaMemcpyAsync(ss, static_cast<const char*>(hs[r]) + off * isz, n * isz,
+                                   cudaMemcpyHostToDevice, c->h2d));
+      sends[r] = ss;
+      recvs[r] = c->stage[4 * r + 2 * slot + 1];
+    }
+    LANE_CUDA(c, cudaEventRecord(c->ev_h[slot], c->h2d));
+    LANE_CUDA(c, cudaStreamWaitEvent(s, c->ev_h[slot], 0));
+    if (i >= 2) LANE_CUDA(c, cudaStreamWaitEvent(s, c->ev_d[slot], 0));  // D2H i-2 read its recv slot
+    st = c->emulated ? lane_allreduce_emulated(c, sends.data(), recvs.data(), n, (lane_dtype_t)dtype,
+                                               (lane_op_t)op, s)
+                     : lane_allreduce(c, sends[0], recvs[0], n, (lane_dtype_t)dtype, (lane_op_t)op, s);
+    if (st != LANE_OK) return st;
+    LANE_CUDA(c, cudaEventRecord(c->ev_k[slot], s));
+    LANE_CUDA(c, cudaStreamWaitEvent(c->d2h, c->ev_k[slot], 0));
+    for (int r = 0; r < nr; ++r)
+      LANE_CUDA(c, cudaMemcpyAsync(static_cast<char*>(hr[r]) + off * isz, recvs[r], n * isz,
+                                   cudaMemcpyDeviceToHost, c->d2h));
+    LANE_CUDA(c, cudaEventRecord(c->ev_d[slot], c->d2h));
+  }
+  LANE_CUDA(c, cudaStreamWaitEvent(s, c->ev_d[(np - 1) & 1], 0));
+  return LANE_OK;
+}
+
 int lane_allreduce_host(lane_comm_t c, const void* host_send, void* host_recv, size_t count,
                         lane_dtype_t dtype, lane_op_t op, void* stream) {
   int st = check_call(c, count, dtype, op);
@@ -624,16 +700,9 @@ int lane_allreduce_host(lane_comm_t c, const void* host_send, void* host_recv, s
   if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_host: use lane_allreduce_emulated_host");
   if (count == 0) return LANE_OK;
   if (!host_send || !host_recv) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
-  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
-  st = ensure_stage(c, bytes);
-  if (st != LANE_OK) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  LANE_CUDA(c, cudaSetDevice(c->device));
-  LANE_CUDA(c, cudaMemcpyAsync(c->stage[0], host_send, bytes, cudaMemcpyHostToDevice, s));
-  st = lane_allreduce(c, c->stage[0], c->stage[1], count, dtype, op, stream);
-  if (st != LANE_OK) return st;
-  LANE_CUDA(c, cudaMemcpyAsync(host_recv, c->stage[1], bytes, cudaMemcpyDeviceToHost, s));
-  return LANE_OK;
+  const void* hs[1] = {host_send};
+  void* hr[1] = {host_recv};
+  return host_pipeline(c, hs, hr, count, dtype, op, static_cast<cudaStream_t>(stream));
 }
 
 int lane_allreduce_emulated_host(lane_comm_t c, const void* const* host_sends,
@@ -644,25 +713,14 @@ int lane_allreduce_emulated_host(lane_comm_t c, const void* const* host_sends,
   if (!c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_emulated_host: comm is not emulated");
   if (count == 0) return LANE_OK;
   if (!host_sends || !host_recvs) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
-  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
-  st = ensure_stage(c, bytes);
-  if (st != LANE_OK) return st;
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
-  LANE_CUDA(c, cudaSetDevice(c->device));
-  std::vector<const void*> sends(c->P);
-  std::vector<void*> recvs(c->P);
-  for (int r = 0; r < c->P; ++r) {
-    if (!host_sends[r] || !host_recvs[r]) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
-    LANE_CUDA(c, cudaMemcpyAsync(c->stage[2 * r], host_sends[r], bytes, cudaMemcpyHostToDevice, s));
-    sends[r] = c->stage[2 * r];
-    recvs[r] = c->stage[2 * r + 1];
-  }
-  st = lane_allreduce_emulated(c, sends.data(), recvs.data(), count, dtype, op, stream);
-  if (st != LANE_OK) return st;
   for (int r = 0; r < c->P; ++r)
-    LANE_CUDA(c, cudaMemcpyAsync(host_recvs[r], c->stage[2 * r + 1], bytes, cudaMemcpyDeviceToHost, s));
-  return LANE_OK;
+    if (!host_sends[r] || !host_recvs[r]) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+  return host_pipeline(c, host_sends, host_recvs, count, dtype, op, static_cast<cudaStream_t>(stream));
 }
+
+}  // extern "C"
+
+extern "C" {
 
 int lane_allreduce_register_handle(lane_comm_t c, void* ptr, size_t bytes, void* blob,
                                    size_t* blob_bytes) {
@@ -748,6 +806,16 @@ void release(lane_comm_t c) {
   for (auto& e : c->ipc_cache) cudaIpcCloseMemHandle(e.second);
   for (char* p : c->own) cudaFree(p);
   for (char* p : c->stage) cudaFree(p);
+  if (c->h2d) {
+    cudaStreamDestroy(c->h2d);
+    cudaStreamDestroy(c->d2h);
+    cudaEventDestroy(c->ev_start);
+    for (int i = 0; i < 2; ++i) {
+      cudaEventDestroy(c->ev_h[i]);
+      cudaEventDestroy(c->ev_k[i]);
+      cudaEventDestroy(c->ev_d[i]);
+    }
+  }
   if (c->abort_dev) cudaFree(c->abort_dev);
   if (c->trace) cudaFree(c->trace);
   if (c->err_host) cudaFreeHost(c->err_host);

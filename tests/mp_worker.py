@@ -86,6 +86,19 @@ def main():
                         print(f"rank {rank} FAIL {N}x{G} k={k} {dtype} n={n} inplace={inplace} reg={registered}: "
                               f"{len(bad)} mismatches first {idx[bad[:5]]}", flush=True)
                         failures += 1
+            # host-buffer API (pipelined pieces, ragged tail)
+            os.environ["LANE_HOST_PIECE_BYTES"] = str(1 << 18)
+            n = (1 << 20) + 5
+            hx = si.generate("float32", "signed", 77 + k, rank, n)
+            hin = torch.from_numpy(hx).pin_memory()
+            hout = torch.empty_like(hin).pin_memory()
+            comm.allreduce_host(hout, hin)
+            ref = oracle.lane_allreduce([si.generate("float32", "signed", 77 + k, p_, n) for p_ in range(P)],
+                                        N, G, 1, "float32").out[0]
+            if not np.array_equal(hout.numpy().view(np.uint32), ref.view(np.uint32)):
+                print(f"rank {rank} FAIL host api {N}x{G} k={k}", flush=True)
+                failures += 1
+            os.environ.pop("LANE_HOST_PIECE_BYTES")
             dist.barrier()
             comm.close()
             dist.barrier()

@@ -154,14 +154,30 @@ def test_errors_misaligned_and_dtype():
     assert ei.value.code == -2
 
 
-def test_host_buffer_api_emulated():
+@pytest.mark.parametrize("piece", [None, 65536, 4096 * 3 + 16])
+def test_host_buffer_api_emulated(piece):
+    """lane_allreduce_emulated_host: pipelined H2D / kernel / D2H in pieces
+    (each piece its own allreduce), including a ragged last piece."""
     import torch
     N, G = 2, 4
-    xs = si.generate_all("float32", "signed", 11, 8, 300001)
-    ins = [torch.from_numpy(x).pin_memory() for x in xs]
-    outs = [torch.empty_like(t).pin_memory() for t in ins]
-    emu(N, G, 1).allreduce_host(outs, ins)
-    assert_parity([o.numpy() for o in outs], xs, N, G, "float32", "host api")
+    old = os.environ.get("LANE_HOST_PIECE_BYTES")
+    if piece:
+        os.environ["LANE_HOST_PIECE_BYTES"] = str(piece)
+    try:
+        for dtype in ("float32", "bfloat16"):
+            xs = si.generate_all(dtype, "signed", 11, 8, 300001)
+            if dtype == "bfloat16":
+                ins = [torch.from_numpy(x.view(np.int16).copy()).view(torch.bfloat16).pin_memory() for x in xs]
+            else:
+                ins = [torch.from_numpy(x).pin_memory() for x in xs]
+            outs = [torch.empty_like(t).pin_memory() for t in ins]
+            emu(N, G, 1).allreduce_host(outs, ins)
+            assert_parity([to_numpy(o, dtype) for o in outs], xs, N, G, dtype, f"host api piece={piece}")
+    finally:
+        if old is None:
+            os.environ.pop("LANE_HOST_PIECE_BYTES", None)
+        else:
+            os.environ["LANE_HOST_PIECE_BYTES"] = old
 
 
 @pytest.mark.parametrize("N,G,k,dtype,n", [
