@@ -622,7 +622,10 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
   p.nlocal = c->P;
-  p.direct = (c->engine == 1 && env_i64("LANE_DIRECT", 1)) ? 1 : 0;
+  // emulated: every buffer is addressable; pull flavour by default (fewest HBM
+  // bytes), LANE_DIRECT=2 runs the push flavour of the multi-GPU path
+  p.direct = c->engine == 1 ? (int)env_i64("LANE_DIRECT", 1) : 0;
+  if (p.direct < 0 || p.direct > 2) p.direct = 1;
   for (int r = 0; r < c->P; ++r) {
     p.rk[r].send = static_cast<const char*>(sendbufs[r]);
     p.rk[r].recv = static_cast<char*>(recvbufs[r]);

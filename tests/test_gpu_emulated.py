@@ -77,12 +77,16 @@ def test_seeded_fill_device_matches_numpy():
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-def test_parity_layouts(N, G, dtype):
+@pytest.mark.parametrize("mode", ["1", "2", "0"])
+def test_parity_layouts(N, G, dtype, mode, monkeypatch):
+    """LANE_DIRECT 1 = direct-pull (emulated default), 2 = direct-push (the
+    registered multi-GPU job set), 0 = staged (the unregistered job set)."""
+    monkeypatch.setenv("LANE_DIRECT", mode)
     for k in (1, 2, 4):
         for n in COUNTS:
             xs = si.generate_all(dtype, "signed", 42 + n, N * G, n)
             got = run(N, G, k, dtype, xs)
-            assert_parity(got, xs, N, G, dtype, f"{N}x{G} k={k} n={n}")
+            assert_parity(got, xs, N, G, dtype, f"{N}x{G} k={k} n={n} mode={mode}")
 
 
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
@@ -94,7 +98,9 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-def test_inplace_and_repeated_calls_epoch_reuse():
+@pytest.mark.parametrize("mode", ["1", "2", "0"])
+def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
+    monkeypatch.setenv("LANE_DIRECT", mode)
     N, G, k = 2, 4, 2
     for it in range(6):
         n = [5000, 1 << 16, 33, 1 << 20, 4097, 1 << 16][it]
