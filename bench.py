@@ -55,6 +55,9 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-nccl", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--nccl-ppg", type=int, default=4,
+                    help="multi-GPU: also time the paper's multi-PPG CCL variant (P L269, L504): this many "
+                         "NCCL communicators, each allreducing a 1/PPG slice on its own stream (0 = skip)")
     ap.add_argument("--no-register", action="store_true",
                     help="multi-GPU: do not register the buffers (staged path through library scratch)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
@@ -434,6 +437,8 @@ def run_multi(args):
         line["e2e"] = e2e_multi(comm, inp, N, G, dtype, n, S, args, dist)
     if not args.no_nccl:
         line["nccl_ring"] = nccl_ring(inp, S, P, args, dist, stream)
+        if args.nccl_ppg > 1:
+            line["nccl_ring_multi_ppg"] = nccl_ppg(inp, S, P, args, dist, stream, NcclPPG(args.nccl_ppg, dist))
     if rank == 0:
         print(json.dumps(line), flush=True)
     comm.close()
@@ -456,6 +461,42 @@ def e2e_multi(comm, inp, N, G, dtype, n, S, args, dist):
     return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 3),
             "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
             "api": "lane_allreduce_host (C ABI, pinned host buffers)"}
+
+
+class NcclPPG:
+    """the paper's multi-PPG CCL approach — PPG communicators per
+    GPU, each running a standard NCCL allreduce on its own 1/PPG slice of the
+    buffer on its own stream (P L269 §2.2, P L504 §4.2)."""
+
+    def __init__(self, ppg, dist):
+        import torch
+        self.ppg = ppg
+        self.groups = [dist.new_group(backend="nccl") for _ in range(ppg)]
+        self.streams = [torch.cuda.Stream() for _ in range(ppg)]
+
+    def run(self, buf, dist):
+        import torch
+        cur = torch.cuda.current_stream()
+        n = buf.numel()
+        q = 4  # slice boundaries on 16 B for fp32/int32 (8 for bf16 is also fine)
+        for i, (g, st) in enumerate(zip(self.groups, self.streams)):
+            a = (n * i // self.ppg) // q * q
+            b = n if i == self.ppg - 1 else (n * (i + 1) // self.ppg) // q * q
+            st.wait_stream(cur)
+            with torch.cuda.stream(st):
+                dist.all_reduce(buf[a:b], group=g)
+        for st in self.streams:
+            cur.wait_stream(st)
+
+
+def nccl_ppg(inp, S, P, args, dist, stream, ppg_obj):
+    import torch
+    buf = inp.clone()
+    ms = device_time_ms(lambda: ppg_obj.run(buf, dist), args.steps, args.warmup, stream, lambda: dist.barrier())
+    t = torch.tensor([ms], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 4),
+            "ppg": ppg_obj.ppg, "algo": os.environ.get("NCCL_ALGO", "default")}
 
 
 def nccl_ring(inp, S, P, args, dist, stream):
@@ -484,6 +525,7 @@ def run_sweep(args):
     P, dtype, isz = world, args.dtype, itemsize(args.dtype)
     comm = lane.LaneComm(N, G, args.k, rank=rank, device=local)
     stream = torch.cuda.current_stream()
+    ppg = NcclPPG(args.nccl_ppg, dist) if args.nccl_ppg > 1 else None
     mib = 1
     rows = []
     while mib <= args.mib:
@@ -499,12 +541,16 @@ def run_sweep(args):
         ok = sample_check([out], N, G, dtype, n, 42, [rank])
         buf = inp.clone()
         ms_n = device_time_ms(lambda: dist.all_reduce(buf), steps, 5, stream, lambda: dist.barrier())
-        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0], dtype=torch.float64)
+        ms_p = device_time_ms(lambda: ppg.run(buf, dist), steps, 5, stream, lambda: dist.barrier()) if ppg else 0.0
+        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0, ms_p], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         row = {"layout": f"{N}x{G}", "k": args.k, "dtype": dtype, "bytes": S, "ms": round(t[0].item(), 4),
                "busbw": round(busbw(S, P, t[0].item()), 2), "nccl_ring_ms": round(t[1].item(), 4),
                "nccl_ring_busbw": round(busbw(S, P, t[1].item()), 2), "verified": t[2].item() == 0,
                "frac_of_770": round(busbw(S, P, t[0].item()) / NVLINK_PEAK, 4), "plan": comm.plan(n, dtype)}
+        if ppg:
+            row["nccl_ring_ppg"] = args.nccl_ppg
+            row["nccl_ring_ppg_busbw"] = round(busbw(S, P, t[3].item()), 2)
         row["registered_buffers"] = bool(regs)
         rows.append(row)
         if rank == 0:
