@@ -47,7 +47,9 @@ constexpr int kThreads = 32 * (2 + kConsumerWarps);  // producer warp, releaser 
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
 constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
-constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 64;
+constexpr int kJobCacheBytes = 5 * 576;  // producer's next job of every phase
+constexpr int kSmemBytes =
+    kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 64 + kJobCacheBytes;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -323,6 +325,7 @@ struct TileDesc {
 
 constexpr int kDescBytes = 320;
 static_assert(sizeof(TileDesc) <= kDescBytes, "TileDesc must fit its smem slot");
+static_assert(sizeof(Job) <= 576, "Job must fit its smem slot");
 
 // A job's flag releases, handed from the storer to the releaser warp.
 struct RelRec {
@@ -336,6 +339,15 @@ struct RelRing {
   volatile int head;  // records retired by the releaser
   volatile int done;  // storer finished (or aborted)
 };
+
+// Relaxed poll (no per-poll fence); a fence_acquire_sys() after the last
+// observation completes the acquire pattern.
+__device__ __forceinline__ bool flag_seen(const LaneParams& p, const uint32_t* f) {
+  uint32_t v;
+  asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+  return (int32_t)(v - p.epoch) >= 0;
+}
+__device__ __forceinline__ void fence_acquire_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ bool flag_ready(const LaneParams& p, const uint32_t* f) {
   return (int32_t)(ld_acquire_sys(f) - p.epoch) >= 0;
@@ -378,6 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
   RelRec* rel_rec = reinterpret_cast<RelRec*>(desc + kStages);
   RelRing* ring = reinterpret_cast<RelRing*>(rel_rec + kRelSlots);
   volatile int* abort_s = reinterpret_cast<volatile int*>(ring + 1);
+  Job* jobs = reinterpret_cast<Job*>(smem + kSmemBytes - kJobCacheBytes);  // producer only
 
   const int per_rank = p.k * p.C;
   Ctx x;
@@ -500,19 +513,25 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       if (ok) fence_async_global();
     }
     uint64_t t_idle = 0;
+    // jobs[ph] (shared memory): next job of every phase, built once per job
+    bool have[5] = {false, false, false, false, false};
+    int wpos[5] = {0, 0, 0, 0, 0};  // flags of jobs[ph] already seen set
     while (ok) {
       int pick = -1;
-      Job J;
       bool any_left = false;
       for (int ph = 0; ph < 5 && pick < 0; ++ph) {
         if (cur[ph] >= m) continue;
         any_left = true;
         if (prev[ph] >= 0 && cur[ph] >= cur[prev[ph]]) continue;  // previous phase not issued yet
         if (ph == 0 && last >= 0 && last != 0 && cur[0] - cur[last] >= window) continue;
-        make_job(x, ph, chunk_geo(p, cb, sl, j + cur[ph] * p.C), sub[ph], J);
-        bool ready = true;
-        for (int w = 0; w < J.nwait && ready; ++w) ready = flag_ready(p, J.wait[w]);
-        if (ready) pick = ph;
+        if (!have[ph]) {
+          make_job(x, ph, chunk_geo(p, cb, sl, j + cur[ph] * p.C), sub[ph], jobs[ph]);
+          have[ph] = true;
+          wpos[ph] = 0;
+        }
+        const Job& Jc = jobs[ph];
+        while (wpos[ph] < Jc.nwait && flag_ready(p, Jc.wait[wpos[ph]])) ++wpos[ph];
+        if (wpos[ph] == Jc.nwait) pick = ph;
       }
       if (!any_left) break;
       if (pick < 0) {  // nothing ready: watchdog + abort checks
@@ -531,7 +550,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
         if (tr) tr_flag += globaltimer_ns() - t_idle;
         t_idle = 0;
       }
-      if (J.nwait) fence_async_global();  // acquire (generic proxy) before async-proxy reads
+      const Job& J = jobs[pick];
+      if (J.nwait) fence_async_global();  // acquired flags ordered before the async-proxy (TMA) reads
+      have[pick] = false;  // J stays valid until the next make_job of this phase
       // advance the phase cursor
       if (++sub[pick] == nj[pick]) {
         sub[pick] = 0;
