@@ -146,6 +146,15 @@ def device_time_ms(fn, steps, warmup, stream, barrier=None):
     return s.elapsed_time(e) / steps
 
 
+def nvlink_bytes(dev):
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from nvlink_counters import nvlink_bytes as nb
+        return nb(dev)
+    except Exception:
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -399,7 +408,12 @@ def run_multi(args):
     clk = Clocks(list(range(world))) if rank == 0 else None
     if clk:
         clk.__enter__()
-    ms = device_time_ms(step, args.steps, args.warmup, stream, barrier)
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    nv0 = nvlink_bytes(local)
+    ms = device_time_ms(step, args.steps, 0, stream, barrier)
+    nv1 = nvlink_bytes(local)
     if clk:
         clk.__exit__()
     comm.check()
@@ -412,6 +426,18 @@ def run_multi(args):
     ok = okt.item() == 0
     bw = busbw(S, P, ms_max)
     launches = max(plan["launches"], 1)
+    # measured NVLink data bytes per launch (NVML counters of this GPU), mean over ranks
+    nv = torch.tensor([-1.0, -1.0], dtype=torch.float64)
+    if nv0 and nv1:
+        nv = torch.tensor([(nv1[0] - nv0[0]) / (args.steps * launches), (nv1[1] - nv0[1]) / (args.steps * launches)],
+                          dtype=torch.float64)
+    nvs = [torch.zeros(2, dtype=torch.float64) for _ in range(world)]
+    dist.all_gather(nvs, nv)
+    tx = [float(v[0]) for v in nvs]
+    rx = [float(v[1]) for v in nvs]
+    nvl = None if min(tx) < 0 else {"tx_bytes_per_launch_mean": sum(tx) / world,
+                                     "rx_bytes_per_launch_mean": sum(rx) / world,
+                                     "tx_over_algorithmic": sum(tx) / world / (2 * (P - 1) / P * S / launches)}
     line = base_line(args, world, args.steps, args.warmup)
     line.update({
         "value": round(bw, 2) if ok else None, "ms_per_step": round(ms_max, 4),
@@ -425,7 +451,10 @@ def run_multi(args):
         "verified": ok,
         "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": NVLINK_PEAK, "unit": "GB/s",
                      "frac": round(bw / NVLINK_PEAK, 4), "frac_of_nominal_900": round(bw / NVLINK_NOMINAL, 4),
-                     "traffic": None,
+                     "traffic": None if nvl is None else int(nvl["tx_bytes_per_launch_mean"]),
+                     "traffic_source": "NVML NVLink data TX counters (mean over ranks; ncu cannot wrap "
+                                       "multi-rank runs)" if nvl else None,
+                     "nvlink_counters": nvl,
                      "peak_source": "measured peer copy per direction, B200_PROFILING.md (no NVLink entry in "
                                     "MEASURED_PEAKS.json)",
                      "algorithmic_bytes_per_launch": int(2 * (P - 1) / P * S / launches)},
