@@ -28,3 +28,4 @@ from .lane_oracle import (  # noqa: F401
     split_remainder_first,
     to_float64,
 )
+from .ring_oracle import RingResult, ring_allreduce, ring_chunks  # noqa: F401,E402

@@ -1,0 +1,119 @@
+"""Pins for the ring allreduce oracle (oracle/ring_oracle.py, Alg. 1).
+
+Checked against things other than itself: the plain definition (exact int64
+sums mod 2^32; float64 sums within the per-hop error bound), the hand-derived
+ring-order fixture tests/golden/ring_order.txt, closed-form byte and message
+counts (2(p-1) messages, P L211; 2(P-1)/P*n elements per rank), and the P = 2
+special case where one commutative add makes the ring and the lane method
+bit-identical.
+"""
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import seeded_inputs as si
+from oracle import lane_oracle as lo
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _cases():
+    with open(os.path.join(GOLDEN, "ring_order.txt")) as f:
+        for line in f:
+            line = line.strip()
+            if line.startswith("case "):
+                yield line
+
+
+def _val(s, dtype):
+    return int(s, 16) if dtype == "bfloat16" else (float(s) if dtype == "float32" else int(s))
+
+
+@pytest.mark.parametrize("line", list(_cases()))
+def test_ring_order_fixture(line):
+    f = line.split()
+    name, dtype, P, n = f[1], f[2], int(f[3]), int(f[4])
+    kv = dict(x.split("=") for x in f[5:])
+    ins = [_val(v, dtype) for v in kv["inputs"].split(",")]
+    exp = [_val(v, dtype) for v in kv["expect"].split(",")]
+    own = [int(v) for v in kv["owners"].split(",")]
+    xs = [np.full(n, v, dtype=lo.STORAGE[dtype]) for v in ins]
+    r = oracle.ring_allreduce(xs, 1, dtype)
+    q = 16 // lo.ITEMSIZE[dtype]
+    for c, (e, o) in enumerate(zip(exp, own)):
+        for p in range(P):
+            got = r.out[p][c * q:(c + 1) * q]
+            assert np.all(got == np.array(e, dtype=lo.STORAGE[dtype])), (name, c, p, got)
+        assert np.all(r.owner[c * q:(c + 1) * q] == o), (name, c)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("k", [1, 3])
+@pytest.mark.parametrize("n", [1, 5, 64, 4099])
+def test_ring_int32_exact_and_identical(P, k, n):
+    xs = si.generate_all("int32", "full", 3, P, n)
+    r = oracle.ring_allreduce(xs, k, "int32")
+    ref = oracle.brute_force_sum(xs, "int32")
+    for o in r.out:
+        assert np.array_equal(o, ref)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+@pytest.mark.parametrize("P", [3, 4, 8])
+def test_ring_fp_error_bound(dtype, P):
+    """fp32: P-1 RNE adds, |err| <= (P-1) 2^-24 sum|x|; bf16 adds one bf16
+    rounding per hop (unit roundoff 2^-8 for 8 significant bits), |err| <=
+    (P-1)(2^-24 + 2^-8) sum|x| (each hop's result
+    is bounded by the partial sum of |x|)."""
+    n = 20011
+    xs = si.generate_all(dtype, "signed", 5, P, n)
+    r = oracle.ring_allreduce(xs, 2, dtype)
+    for o in r.out[1:]:
+        assert np.array_equal(o.view(np.uint8), r.out[0].view(np.uint8))
+    ref = oracle.brute_force_sum(xs, dtype)
+    err = np.abs(oracle.to_float64(r.out[0], dtype) - ref)
+    u = 2.0 ** -24 + (2.0 ** -8 if dtype == "bfloat16" else 0.0)
+    assert np.all(err <= (P - 1) * u * oracle.abs_sum(xs, dtype) * (1 + 1e-9))
+
+
+def test_ring_bf16_per_hop_differs_from_single_rounding():
+    """R#11: the ring rounds every hop; the lane method rounds once per phase.
+    On the fixture's inputs the two disagree (1.0 vs 1+2^-7)."""
+    xs = [np.full(8, v, np.uint16) for v in (0x3F80, 0x3B80, 0x3B80)]
+    ring = oracle.ring_allreduce(xs, 1, "bfloat16").out[0]
+    lane = oracle.lane_allreduce(xs, 1, 3, 1, "bfloat16").out[0]
+    assert ring[0] == 0x3F80 and lane[0] == 0x3F81
+
+
+@pytest.mark.parametrize("P,k,n", [(2, 1, 4096), (4, 1, 4096), (8, 2, 1 << 14), (3, 1, 12)])
+def test_ring_ledger_closed_forms(P, k, n):
+    """Alg. 1 sends 2(p-1) messages (P L211); with n divisible by 4*k*P every
+    rank sends and receives 2(P-1)/P * n elements."""
+    xs = si.generate_all("int32", "signed", 1, P, n)
+    r = oracle.ring_allreduce(xs, k, "int32")
+    assert np.all(r.messages == 2 * (P - 1) * k)
+    assert np.all(r.sent == 2 * (P - 1) * n // P)
+    assert np.all(r.recv == 2 * (P - 1) * n // P)
+    # chunk c completes on rank c-1 (the last rp of the reduce-scatter loop)
+    for l, D in enumerate(oracle.ring_chunks(n, 4, P, k)):
+        for c, (s, e) in enumerate(D):
+            assert np.all(r.owner[s:e] == (c - 1) % P)
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16", "int32"])
+def test_ring_p2_equals_lane(dtype):
+    """P = 2: every element is one commutative add in both algorithms."""
+    xs = si.generate_all(dtype, "signed", 9, 2, 777)
+    ring = oracle.ring_allreduce(xs, 2, dtype).out[0]
+    for N, G in ((1, 2), (2, 1)):
+        lane = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
+        assert np.array_equal(ring.view(np.uint8), lane.view(np.uint8))
+
+
+def test_ring_p1_and_empty():
+    x = si.generate("float32", "signed", 1, 0, 33)
+    assert np.array_equal(oracle.ring_allreduce([x], 1, "float32").out[0], x)
+    r = oracle.ring_allreduce([np.zeros(0, np.float32)] * 3, 2, "float32")
+    assert all(len(o) == 0 for o in r.out)
