@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-register", action="store_true",
                     help="multi-GPU: do not register the buffers (staged path through library scratch)")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ring", action="store_true",
+                    help="sweep: also time the library's ring allreduce (Alg. 1, the paper's standard algorithm)")
     ap.add_argument("--sweep", default=None,
                     help="multi-GPU: write busbw vs message size (ours and NCCL ring) as JSONL to this file")
     return ap.parse_args()
@@ -241,6 +243,32 @@ def sample_check(outs, N, G, dtype, n, seed, ranks):
         if not np.array_equal(got, ref.view(vb)):
             return False
     return True
+
+
+def ring_check(out, P, k, dtype, n, seed, plan):
+    """Check of the ring allreduce's output (Alg. 1 order, per-hop rounding):
+    bit-exact against the ring oracle with the library's chunk plan when the
+    whole message is small enough for the oracle; above that, the first 2^16
+    elements against the plain sum within the per-hop error bound."""
+    import numpy as np
+    import torch
+    import oracle
+    import seeded_inputs as si
+    m = min(n, 1 << 16)  # the first m elements: a full prefix when n == m, else an exact int check
+    idx = np.arange(m)
+    xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(P)]
+    got = out[:m].cpu()
+    got = (got.view(torch.int16).numpy() if dtype == "bfloat16" else got.view(torch.int32).numpy())
+    if m == n:
+        ref = oracle.ring_allreduce(xs, k, dtype, plan["chunk_granules"], plan["round_granules"]).out[0]
+        return np.array_equal(got.view(np.uint16 if dtype == "bfloat16" else np.uint32),
+                              ref.view(np.uint16 if dtype == "bfloat16" else np.uint32))
+    ref = oracle.brute_force_sum(xs, dtype)
+    if dtype == "int32":
+        return np.array_equal(got, ref)
+    err = np.abs(oracle.to_float64(got.view(np.uint16) if dtype == "bfloat16" else got.view(np.float32), dtype) - ref)
+    u = 2.0 ** -24 + (2.0 ** -8 if dtype == "bfloat16" else 0.0)
+    return bool(np.all(err <= (P - 1) * u * oracle.abs_sum(xs, dtype) * (1 + 1e-9)))
 
 
 def base_line(args, N_gpus, K, W):
@@ -571,12 +599,21 @@ def run_sweep(args):
         buf = inp.clone()
         ms_n = device_time_ms(lambda: dist.all_reduce(buf), steps, 5, stream, lambda: dist.barrier())
         ms_p = device_time_ms(lambda: ppg.run(buf, dist), steps, 5, stream, lambda: dist.barrier()) if ppg else 0.0
-        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0, ms_p], dtype=torch.float64)
+        ms_r, ok_r = 0.0, True
+        if args.ring:  # Alg. 1 ring on the same comm (standard approach with k slices)
+            ms_r = device_time_ms(lambda: comm.allreduce_ring(out, inp), steps, 5, stream, lambda: dist.barrier())
+            ok_r = ring_check(out, P, args.k, dtype, n, 42, comm.plan(n, dtype, algorithm="ring"))
+            ok = ok and ok_r
+        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0, ms_p, ms_r], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         row = {"layout": f"{N}x{G}", "k": args.k, "dtype": dtype, "bytes": S, "ms": round(t[0].item(), 4),
                "busbw": round(busbw(S, P, t[0].item()), 2), "nccl_ring_ms": round(t[1].item(), 4),
                "nccl_ring_busbw": round(busbw(S, P, t[1].item()), 2), "verified": t[2].item() == 0,
                "frac_of_770": round(busbw(S, P, t[0].item()) / NVLINK_PEAK, 4), "plan": comm.plan(n, dtype)}
+        if args.ring:
+            row["lane_ring_alg1_busbw"] = round(busbw(S, P, t[4].item()), 2)
+            row["lane_ring_alg1_ms"] = round(t[4].item(), 4)
+        row["protocol"] = comm.protocol(n, dtype)
         if ppg:
             row["nccl_ring_ppg"] = args.nccl_ppg
             row["nccl_ring_ppg_busbw"] = round(busbw(S, P, t[3].item()), 2)

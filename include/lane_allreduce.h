@@ -144,6 +144,38 @@ int lane_allreduce_emulated_host(lane_comm_t comm, const void* const* host_sends
                                  void* const* host_recvs, size_t count, lane_dtype_t dtype,
                                  lane_op_t op, void* stream);
 
+/* ---------------------------------------------------- ring (Alg. 1) baseline
+ * The paper's "standard" allreduce, Alg. 1 ring_allreduce (PAPER.md
+ * L150-206): a flat ring over all P = N*G ranks (rank r sends to r+1),
+ * P-1 reduce-scatter steps then P-1 allgather steps; with the comm's k it is
+ * the paper's "standard approach" with k processes per GPU (§3.1.1, P
+ * L335-349: every k-slice is ring-allreduced independently). Hand-written
+ * sm_100a kernel on the LL protocol (see LANE_PROTO_LL); messages above
+ * $LANE_LL_MAX_BYTES run in several launches. Unlike lane_allreduce, each
+ * chunk is reduced in ring order starting at rank c with one rounding per
+ * hop in the buffer type (bf16: per-hop RNE, R#11), so results
+ * differ in the last bits from the multi-lane method (int32: identical).
+ * Same argument rules and errors as lane_allreduce / _emulated; buffers need
+ * no registration. */
+int lane_allreduce_ring(lane_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                        lane_dtype_t dtype, lane_op_t op, void* stream);
+int lane_allreduce_ring_emulated(lane_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
+                                 size_t count, lane_dtype_t dtype, lane_op_t op, void* stream);
+
+/* The ring's plan for (count, dtype), as lane_allreduce_plan: the pipeline
+ * chunk ($LANE_RING_CHUNK_BYTES, default 64 KiB; every chunk of every k-slice
+ * is its own Alg. 1 ring, R#21), the round size ($LANE_LL_MAX_BYTES)
+ * in granules, CTAs per CTA group and launches. Any out-pointer may be NULL.
+ *
+ * $LANE_PHASE2=ring (read at init) switches lane_allreduce to the paper's
+ * variant with the ring as the inter-node stage (fig:full_mpi_comparison,
+ * P L401, L457): phase 1 and 3 unchanged, phase 2 = Alg. 1 among the N lane
+ * members on every group part (its N sub-parts are the ring chunks), one
+ * rounding per hop; it runs on the LL protocol with the same fixed chunking,
+ * reported by lane_allreduce_plan. */
+int lane_allreduce_ring_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype, int64_t* chunk_granules,
+                             int64_t* round_granules, int* ctas_per_group, int* launches);
+
 /* ----------------------------------------------------------------- common */
 
 /* Release scratch, IPC mappings and staging. Collective in multi-GPU mode:
@@ -172,6 +204,23 @@ int lane_allreduce_trace(lane_comm_t comm, uint64_t* out, size_t max_words, size
 int lane_allreduce_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype,
                         int64_t* chunk_granules, int64_t* round_granules, int* ctas_per_group,
                         int* launches);
+
+/* Signalling protocol of a call (both compute the same method and the same
+ * bits). SIMPLE: one persistent kernel moves chunk tiles through a TMA
+ * pipeline and publishes per-job epoch flags after a system-scope fence
+ * (large messages; §3.1.2 phases as chunked jobs). LL: every 16-byte
+ * granule travels as a 32-byte packet of four {data, epoch} 64-bit words, so
+ * the reader's poll on the data is the signal (no fences; 2x NVLink bytes;
+ * used up to $LANE_LL_THRESHOLD_BYTES, default 8 MiB per rank, and at most
+ * $LANE_LL_MAX_BYTES, default 16 MiB, the LL inbox capacity;
+ * $LANE_PROTO = ll | simple forces one). */
+#define LANE_PROTO_SIMPLE 0
+#define LANE_PROTO_LL 1
+
+/* *protocol receives the protocol lane_allreduce uses for (count, dtype) on
+ * this comm (LANE_PROTO_SIMPLE for count 0 and P == 1). Errors: INVALID_ARG
+ * (null), UNSUPPORTED (dtype). Host only. */
+int lane_allreduce_protocol(lane_comm_t comm, size_t count, lane_dtype_t dtype, int* protocol);
 
 /* -------------------------------------------------- host-only introspection
  * No GPU needed; used by the CPU test-suite to compare the library's own

@@ -249,12 +249,21 @@ class OracleResult:
 # --------------------------------------------------------------------------
 def lane_allreduce(xs, N: int, G: int, k: int = 1, dtype: str = "float32",
                    chunk_granules: int | None = None,
-                   round_granules: int | None = None) -> OracleResult:
+                   round_granules: int | None = None,
+                   phase2: str = "direct") -> OracleResult:
     """Simulate the P = N*G ranks of the k-split multi-lane allreduce.
 
     ``xs``: list of P input arrays (storage dtype: int32 / float32 / uint16 for
     bf16 bits), all of length n. Returns per-rank outputs plus the ledger and
-    ownership maps. Follows O1-O7 above in the paper's phase order."""
+    ownership maps. Follows O1-O7 above in the paper's phase order.
+
+    ``phase2``: the lane stage's inner algorithm. "direct" (R#5): each owner
+    reduces its sub-part over the lane in ascending b, then an allgather.
+    "ring": the variant of fig:full_mpi_comparison (P L401, L457, "the ring
+    algorithm is used in the inter-node stage"): Alg. 1 among the N lane
+    members on every group part, whose N sub-parts are the ring chunks; ring
+    chunk t starts on node t and completes on node t-1, one rounding per hop
+    (R#11)."""
     topo = Topology(N, G, k)  # O1
     P = topo.P
     if len(xs) != P:
@@ -291,7 +300,11 @@ def lane_allreduce(xs, N: int, G: int, k: int = 1, dtype: str = "float32",
     # O4 phase 2 reduce-scatter on comm_lane (P L246, R#5): the owner (a, g)
     # of unit U(g, a) sums T1 of every node b in ascending b, one rounding.
     F = np.zeros(n, STORAGE[dtype])
-    for u in units:
+    if phase2 == "ring":
+        _phase2_ring(T1, F, units, topo, dtype, ledger, phase2_owner)
+    elif phase2 != "direct":
+        raise ValueError(phase2)
+    for u in units if phase2 == "direct" else []:
         s, e = u.start, u.end
         owner = topo.rank(u.a, u.g)
         acc = widen(T1[0][s:e], dtype)
@@ -303,17 +316,19 @@ def lane_allreduce(xs, N: int, G: int, k: int = 1, dtype: str = "float32",
             ledger.move("phase2_rs", topo.rank(b, u.g), owner, e - s)
 
     # O5 phase 2 allgather on comm_lane: every (b, g) receives F[U(g, a)].
+    # (ring variant: the ring's allgather loop, ledger in _phase2_ring)
     # R[p] is rank p's copy of its group parts after the lane allreduce
     # (Alg. 2: "MPI_Allreduce to buf_recv at offset r(c_group)", P L246).
     SENT = _sentinel(dtype)
     R = [np.full(n, SENT, STORAGE[dtype]) for _ in range(P)]
     for u in units:
         s, e = u.start, u.end
-        owner = topo.rank(u.a, u.g)
+        owner = phase2_owner[s] if e > s else topo.rank(u.a, u.g)
         for b in range(N):
             dst = topo.rank(b, u.g)
             R[dst][s:e] = F[s:e]
-            ledger.move("phase2_ag", owner, dst, e - s)
+            if phase2 == "direct":
+                ledger.move("phase2_ag", owner, dst, e - s)
 
     # O6 phase 3: intra-node allgatherv on comm_group (P L248, "using D"):
     # rank (a, g') receives group part g from (a, g) for every g.
@@ -327,6 +342,35 @@ def lane_allreduce(xs, N: int, G: int, k: int = 1, dtype: str = "float32",
                 ledger.move("phase3", src, dst, e - s)
 
     return OracleResult(out, ledger, phase1_owner, phase2_owner, units, T1, F)
+
+
+def _phase2_ring(T1, F, units, topo, dtype, ledger, phase2_owner):
+    """O4+O5, ring variant: Alg. 1 (P L150-206) on comm_lane for every group
+    part. The part's N units (sub-parts a = 0..N-1) are the ring chunks.
+    Reduce-scatter step i: node b sends chunk b-i to b+1, which adds its own
+    T1 chunk in ONE rounding (MPI_Reduce); chunk t therefore accumulates
+    T1_t, T1_{t+1}, ..., T1_{t-1} and completes on node t-1. The allgather
+    loop then gives every lane member every chunk (N-1 steps)."""
+    N = topo.nodes
+    groups = {}
+    for u in units:
+        groups.setdefault((u.round, u.l, u.c, u.g), []).append(u)
+    for (_, _, _, g), us in groups.items():
+        for t, u in enumerate(us):  # ring chunk t = sub-part a = t
+            s, e = u.start, u.end
+            cur = T1[t][s:e].copy()
+            for i in range(1, N):
+                b = (t + i) % N  # the node that receives the partial from b-1 and adds its own
+                cur = narrow(add(widen(cur, dtype), widen(T1[b][s:e], dtype), dtype), dtype)
+            F[s:e] = cur
+            phase2_owner[s:e] = topo.rank((t - 1) % N, g)
+        # ledger: N-1 reduce-scatter steps, then N-1 allgather steps
+        for i in range(N - 1):
+            for b in range(N):
+                u = us[(b - i) % N]
+                ledger.move("phase2_rs", topo.rank(b, g), topo.rank((b + 1) % N, g), u.end - u.start)
+                u = us[(b + 1 - i) % N]
+                ledger.move("phase2_ag", topo.rank(b, g), topo.rank((b + 1) % N, g), u.end - u.start)
 
 
 def _sentinel(dtype: str):

@@ -48,16 +48,31 @@ class RingResult:
     messages: np.ndarray   # messages sent per rank
 
 
-def ring_chunks(n: int, itemsize: int, P: int, k: int = 1) -> list[list[tuple[int, int]]]:
-    """Element ranges [start, end) of ring chunk c of k-slice l: slices are the
-    remainder-first split of the message's 16-byte granules into k (R#3), ring
-    chunks the remainder-first split of a slice into P (R#2); clipped at n."""
+def ring_chunks(n: int, itemsize: int, P: int, k: int = 1, chunk_granules: int | None = None,
+                round_granules: int | None = None) -> list[list[tuple[int, int]]]:
+    """The independent rings of a message: for every (round, k-slice, pipeline
+    chunk), the element ranges [start, end) of its P ring chunks. Rounds are
+    consecutive pieces of ``round_granules`` 16-byte granules, slices the
+    remainder-first split of a round into k (R#3), pipeline chunks
+    consecutive pieces of ``chunk_granules`` of a slice (R#21: Alg. 1 runs on
+    every pipeline chunk; None = the whole slice, the paper's one-shot
+    form), ring chunks the remainder-first split of a pipeline chunk into P
+    (R#2); clipped at n. Same hierarchy as ``lane_oracle.partition``."""
     q = GRANULE_BYTES // itemsize
     ng = -(-n // q)
     out = []
-    for s0, slen in split_remainder_first(ng, k):
-        out.append([(min((s0 + c0) * q, n), min((s0 + c0 + cl) * q, n))
-                    for c0, cl in split_remainder_first(slen, P)])
+    if ng == 0:
+        return out
+    rg = round_granules or ng
+    for r0 in range(0, ng, rg):
+        rlen = min(rg, ng - r0)
+        for s0, slen in split_remainder_first(rlen, k):
+            cg = chunk_granules or max(slen, 1)
+            for c0 in range(0, slen, cg):
+                clen = min(cg, slen - c0)
+                base = r0 + s0 + c0
+                out.append([(min((base + p0) * q, n), min((base + p0 + pl) * q, n))
+                            for p0, pl in split_remainder_first(clen, P)])
     return out
 
 
@@ -67,8 +82,10 @@ def _hop(incoming: np.ndarray, own: np.ndarray, dtype: str) -> np.ndarray:
         return narrow(widen(incoming, dtype) + widen(own, dtype), dtype)
 
 
-def ring_allreduce(xs, k: int = 1, dtype: str = "float32") -> RingResult:
-    """Simulate Alg. 1 on every k-slice of the P = len(xs) ranks' buffers."""
+def ring_allreduce(xs, k: int = 1, dtype: str = "float32", chunk_granules: int | None = None,
+                   round_granules: int | None = None) -> RingResult:
+    """Simulate Alg. 1 on every independent ring (k-slice, or pipeline chunk
+    of a slice, see ``ring_chunks``) of the P = len(xs) ranks' buffers."""
     P = len(xs)
     xs = [np.asarray(x, dtype=STORAGE[dtype]) for x in xs]
     n = len(xs[0])
@@ -81,7 +98,7 @@ def ring_allreduce(xs, k: int = 1, dtype: str = "float32") -> RingResult:
     owner = np.full(n, -1, np.int64)
     if P == 1:
         return RingResult([xs[0].copy()], sent, got, np.zeros(n, np.int64), msgs)
-    for D in ring_chunks(n, ITEMSIZE[dtype], P, k):
+    for D in ring_chunks(n, ITEMSIZE[dtype], P, k, chunk_granules, round_granules):
         # reduce-scatter loop (P L175-188)
         sp = list(range(P))
         rp = [(r - 1) % P for r in range(P)]

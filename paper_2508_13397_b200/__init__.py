@@ -80,14 +80,24 @@ def partition_units(count: int, itemsize: int, nodes: int, gpus_per_node: int, p
 class _CommBase:
     _comm = None
 
-    def plan(self, count: int, dtype: str = "float32") -> dict:
+    def plan(self, count: int, dtype: str = "float32", algorithm: str = "lane") -> dict:
+        """Launch plan of ``allreduce`` (algorithm="lane") or ``allreduce_ring``
+        ("ring"): chunk / round granules, CTAs per CTA group, launches."""
         lib = _lib.load()
         cg, rg = ctypes.c_int64(), ctypes.c_int64()
         C, launches = ctypes.c_int(), ctypes.c_int()
-        _lib.check(lib.lane_allreduce_plan(self._comm, count, DTYPE[dtype], ctypes.byref(cg), ctypes.byref(rg),
-                                           ctypes.byref(C), ctypes.byref(launches)), self._comm)
+        fn = lib.lane_allreduce_ring_plan if algorithm == "ring" else lib.lane_allreduce_plan
+        _lib.check(fn(self._comm, count, DTYPE[dtype], ctypes.byref(cg), ctypes.byref(rg),
+                      ctypes.byref(C), ctypes.byref(launches)), self._comm)
         return {"chunk_granules": cg.value, "round_granules": rg.value, "ctas_per_group": C.value,
                 "launches": launches.value}
+
+    def protocol(self, count: int, dtype: str = "float32") -> str:
+        """'ll' or 'simple': the signalling protocol a call of this size uses."""
+        pr = ctypes.c_int()
+        _lib.check(_lib.load().lane_allreduce_protocol(self._comm, count, DTYPE[dtype], ctypes.byref(pr)),
+                   self._comm)
+        return "ll" if pr.value == 1 else "simple"
 
     TRACE_FIELDS = ("prod_total", "prod_flag_wait", "prod_empty_wait", "prod_tiles", "store_total",
                     "store_full_wait", "store_sync", "store_read_wait", "store_flush", "store_jobs",
@@ -162,6 +172,21 @@ class LaneComm(_CommBase):
             raise LaneError(-1, "out: must match inp in numel and dtype")
         code = _lib.load().lane_allreduce(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
                                           _dtype_code(inp), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return out
+
+    def allreduce_ring(self, out, inp, op: str = "sum", stream=None):
+        """The paper's "standard" ring allreduce (Alg. 1; with k > 1 the
+        standard multi-PPG approach): same contract as ``allreduce``, ring
+        reduction order with per-hop rounding."""
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        _check_dev_tensor(inp, self.device, "inp")
+        _check_dev_tensor(out, self.device, "out")
+        if out.numel() != inp.numel() or out.dtype != inp.dtype:
+            raise LaneError(-1, "out: must match inp in numel and dtype")
+        code = _lib.load().lane_allreduce_ring(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
+                                               _dtype_code(inp), 0, _stream_handle(stream))
         _lib.check(code, self._comm)
         return out
 
@@ -244,6 +269,19 @@ class LaneEmulator(_CommBase):
             raise LaneError(-1, "all tensors must have the same numel and dtype")
         code = _lib.load().lane_allreduce_emulated(self._comm, self._ptrs(inps, "inps"), self._ptrs(outs, "outs"),
                                                    n, _dtype_code(inps[0]), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return outs
+
+    def allreduce_ring(self, outs, inps, op: str = "sum", stream=None):
+        """Ring allreduce (Alg. 1) of all emulated ranks."""
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        n = inps[0].numel()
+        if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
+            raise LaneError(-1, "all tensors must have the same numel and dtype")
+        code = _lib.load().lane_allreduce_ring_emulated(self._comm, self._ptrs(inps, "inps"),
+                                                        self._ptrs(outs, "outs"), n, _dtype_code(inps[0]), 0,
+                                                        _stream_handle(stream))
         _lib.check(code, self._comm)
         return outs
 

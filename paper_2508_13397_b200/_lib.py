@@ -53,6 +53,10 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_host": (I, [P, P, P, SZ, I, I, P]),
         "lane_allreduce_emulated": (I, [P, PP, PP, SZ, I, I, P]),
         "lane_allreduce_emulated_host": (I, [P, PP, PP, SZ, I, I, P]),
+        "lane_allreduce_ring": (I, [P, P, P, SZ, I, I, P]),
+        "lane_allreduce_ring_emulated": (I, [P, PP, PP, SZ, I, I, P]),
+        "lane_allreduce_ring_plan": (I, [P, SZ, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
+                                         ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_allreduce_finalize": (I, [P]),
         "lane_allreduce_register_handle": (I, [P, P, SZ, P, ctypes.POINTER(SZ)]),
         "lane_allreduce_register_open": (I, [P, P, SZ, ctypes.POINTER(I)]),
@@ -62,6 +66,7 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_trace": (I, [P, ctypes.POINTER(U64), SZ, ctypes.POINTER(SZ)]),
         "lane_allreduce_plan": (I, [P, SZ, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
+        "lane_allreduce_protocol": (I, [P, SZ, I, ctypes.POINTER(I)]),
         "lane_topology_query": (I, [I, I, I, ctypes.POINTER(I), ctypes.POINTER(I),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_partition_query": (I, [U64, I, I, I, I, I64, I64, ctypes.POINTER(I64), U64,

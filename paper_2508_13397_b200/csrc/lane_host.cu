@@ -22,6 +22,7 @@
 
 #include "../../include/lane_allreduce.h"
 #include "lane_kernels.cuh"
+#include "lane_ll.cuh"
 #include "lane_tma.cuh"
 #include "lane_plan.h"
 
@@ -61,7 +62,8 @@ struct lane_comm_s {
   bool connected = false;
   int threads = 512;
   int engine = 1;           // 0 = LSU (ld/st.global), 1 = TMA bulk pipeline
-  bool lsu_store = true;    // TMA engine: consumers store with st.global (else bulk stores)
+  int store_mode = 0;       // TMA engine stores: 0 auto (bulk from bulk_min), 1 st.global, 2 bulk
+  int64_t bulk_min = 0;     // granules: auto mode uses bulk (TMA) stores from this message size
   int ctas_per_group = 0;  // 0 = choose per call
   int max_coresident = 0;  // CTAs of the kernel that fit on the device at once
   int sm_count = 0;
@@ -70,6 +72,19 @@ struct lane_comm_s {
   int chunks_per_cta = 4;
   int64_t chunk_cap = 0;   // max chunks per round (flag capacity per flag type)
   uint64_t s1_bytes = 0, s2_bytes = 0, r_bytes = 0, flag_bytes = 0, total_bytes = 0;
+  // LL protocol (lane_ll.cuh): message capacity, minimum chunk, inbox geometry
+  int proto = 0;             // 0 = auto, 1 = always LL (when it fits), 2 = never LL
+  int64_t ll_max = 0;        // granules: largest message the LL inboxes hold
+  int64_t ll_thresh = 0;     // granules: auto mode uses LL up to this size
+  int64_t ll_cg_min = 0;     // granules
+  int ll_ctas = 0;           // CTAs per rank for LL launches (0 = SM count)
+  int ll_coresident = 0;     // co-resident CTAs of the LL kernel on the device
+  int64_t ll_slot_g = 0, ll_slot_u = 0;
+  int64_t ring_slot = 0;     // granules per ring RS/AG slot (Alg. 1 on the LL protocol)
+  int64_t ring_cg = 0;       // granules per pipeline chunk of the ring algorithms (fixed, R#21)
+  bool phase2_ring = false;  // LANE_PHASE2=ring: lane method with a ring inter-node stage
+  int64_t ll_set = 0;        // granules per LL parity set (max of the lane and ring layouts)
+  uint64_t ll_bytes = 0;
   std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
   std::vector<void*> opened; // IPC-opened peer allocations
   RankMem rk[LANE_MAX_RANKS];
@@ -150,7 +165,29 @@ void size_scratch(lane_comm_t c) {
   c->s2_bytes = al(c->s2_bytes);
   c->r_bytes = al(c->r_bytes);
   c->flag_bytes = al(c->flag_bytes);
-  c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes;
+  // LL inboxes: a slot holds cap chunks of ceil(CG/G) (ceil(CG/(GN)),
+  // ceil(CG/P) for the flat ring) granules. With CG >= ll_cg_min a round of
+  // M granules has at most M/CG + k chunks, so cap * ceil(CG/G) <= M/G +
+  // M/CG + k*CG/G + k; CG <= ceil(M/k) bounds the k*CG/G term by (M+k)/G.
+  const int64_t M = c->ll_max;
+  if (M > 0) {
+    // (checked by brute force over M, G, N, k, CG in the design notes)
+    const int64_t chunks = M / c->ll_cg_min + k + 1;
+    int64_t cgmax = lane::ceil_div(M, k);
+    if (cgmax < c->ring_cg) cgmax = c->ring_cg;
+    if (cgmax < c->ll_cg_min) cgmax = c->ll_cg_min;
+    c->ll_slot_g = lane::ceil_div(M, G) + chunks + k * (lane::ceil_div(cgmax, G) + 1) + 16;
+    c->ll_slot_u = lane::ceil_div(M, G * N) + 2 * chunks + k * (lane::ceil_div(cgmax, G * N) + 2) + 16;
+    c->ring_slot = lane::ceil_div(M, G * N) + chunks + k * (lane::ceil_div(cgmax, G * N) + 1) + 16;
+    const int64_t lane_set = lane::ll::set_granules((int)G, (int)N, c->ll_slot_g, c->ll_slot_u);
+    const int64_t ring_set = lane::ll::ring_set_granules((int)(G * N), c->ring_slot);
+    c->ll_set = lane_set > ring_set ? lane_set : ring_set;
+    c->ll_bytes = al((uint64_t)(2 * c->ll_set) * lane::ll::kPacketBytes);
+  } else {
+    c->ll_slot_g = c->ll_slot_u = c->ring_slot = c->ll_set = 0;
+    c->ll_bytes = 0;
+  }
+  c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes;
 }
 
 void carve(lane_comm_t c, char* base, RankMem* m) {
@@ -158,6 +195,7 @@ void carve(lane_comm_t c, char* base, RankMem* m) {
   m->s2 = base + c->s1_bytes;
   m->r = base + c->s1_bytes + c->s2_bytes;
   m->flags = reinterpret_cast<uint32_t*>(base + c->s1_bytes + c->s2_bytes + c->r_bytes);
+  m->ll = c->ll_bytes ? base + c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes : nullptr;
   m->send = nullptr;
   m->recv = nullptr;
 }
@@ -178,6 +216,13 @@ int occupancy_of(int engine, int threads) {
   return nb;
 }
 
+template <int DT>
+int ll_occupancy_of() {
+  int nb = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::ll::lane_ll_kernel<DT>, lane::ll::kThreads, 0);
+  return nb;
+}
+
 thread_local std::string g_init_error;  // errors of init calls that return no comm
 
 int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, bool emulated) {
@@ -193,7 +238,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     const char* e = getenv("LANE_ENGINE");
     c->engine = (e && strcmp(e, "lsu") == 0) ? 0 : 1;
     const char* st = getenv("LANE_STORE");
-    c->lsu_store = !(st && strcmp(st, "bulk") == 0);
+    c->store_mode = !st ? 0 : (strcmp(st, "lsu") == 0 ? 1 : (strcmp(st, "bulk") == 0 ? 2 : 0));
   }
   if (c->threads < 64 || c->threads > 512 || c->threads % 32)
     return fail(c, LANE_ERR_INVALID_ARG, "LANE_THREADS must be a multiple of 32 in [64, 512]");
@@ -207,6 +252,23 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   if (c->cg_min < 16) c->cg_min = 16;
   if (c->cg_max < c->cg_min) c->cg_max = c->cg_min;
   c->timeout_ns = (uint64_t)env_i64("LANE_TIMEOUT_MS", 20000) * 1000000ull;
+  {
+    const char* pr = getenv("LANE_PROTO");
+    c->proto = !pr ? 0 : (strcmp(pr, "ll") == 0 ? 1 : (strcmp(pr, "simple") == 0 ? 2 : 0));
+  }
+  c->ll_max = env_i64("LANE_LL_MAX_BYTES", 16 << 20) / 16;
+  if (c->ll_max < 0) c->ll_max = 0;
+  c->ll_thresh = env_i64("LANE_LL_THRESHOLD_BYTES", 8 << 20) / 16;
+  c->ll_cg_min = env_i64("LANE_LL_MIN_CHUNK_BYTES", 4 << 10) / 16;
+  if (c->ll_cg_min < 16) c->ll_cg_min = 16;
+  c->ll_ctas = (int)env_i64("LANE_LL_CTAS", 0);
+  c->bulk_min = env_i64("LANE_BULK_MIN_BYTES", 256 << 20) / 16;
+  c->ring_cg = env_i64("LANE_RING_CHUNK_BYTES", 64 << 10) / 16;
+  if (c->ring_cg < c->ll_cg_min) c->ring_cg = c->ll_cg_min;
+  {
+    const char* p2 = getenv("LANE_PHASE2");
+    c->phase2_ring = p2 && strcmp(p2, "ring") == 0;
+  }
   size_scratch(c);
 
   LANE_CUDA(c, cudaSetDevice(device));
@@ -217,6 +279,12 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   occ = occ < o2 ? occ : o2;
   if (occ < 1) occ = 1;
   c->max_coresident = occ * c->sm_count;
+  {
+    int l0 = ll_occupancy_of<0>(), l1 = ll_occupancy_of<1>(), l2 = ll_occupancy_of<2>();
+    int lo = l0 < l1 ? l0 : l1;
+    lo = lo < l2 ? lo : l2;
+    c->ll_coresident = (lo < 1 ? 1 : lo) * c->sm_count;
+  }
 
   const int nalloc = emulated ? c->P : 1;
   for (int i = 0; i < nalloc; ++i) {
@@ -224,7 +292,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     LANE_CUDA(c, cudaMalloc(&p, c->total_bytes));
     c->own.push_back(p);
     // flags must read 0 before any peer can write an epoch >= 1
-    LANE_CUDA(c, cudaMemset(p + c->s1_bytes + c->s2_bytes + c->r_bytes, 0, c->flag_bytes));
+    LANE_CUDA(c, cudaMemset(p + c->s1_bytes + c->s2_bytes + c->r_bytes, 0, c->flag_bytes + c->ll_bytes));
   }
   LANE_CUDA(c, cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   memset(c->err_host, 0, 64);
@@ -232,8 +300,9 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   LANE_CUDA(c, cudaMalloc(&c->abort_dev, 64));
   LANE_CUDA(c, cudaMemset(c->abort_dev, 0, 64));
   if (env_i64("LANE_TRACE", 0)) {
-    LANE_CUDA(c, cudaMalloc(&c->trace, (size_t)c->max_coresident * lane::kTraceWords * 8));
-    LANE_CUDA(c, cudaMemset(c->trace, 0, (size_t)c->max_coresident * lane::kTraceWords * 8));
+    const size_t nt = (size_t)(c->max_coresident > c->ll_coresident ? c->max_coresident : c->ll_coresident);
+    LANE_CUDA(c, cudaMalloc(&c->trace, nt * lane::kTraceWords * 8));
+    LANE_CUDA(c, cudaMemset(c->trace, 0, nt * lane::kTraceWords * 8));
   }
   LANE_CUDA(c, cudaDeviceSynchronize());
   if (emulated) {
@@ -276,7 +345,36 @@ bool overlaps_partially(const void* s, const void* r, uint64_t bytes) {
 struct Plan {
   int64_t ng, cg, round_len0;
   int rounds, C, tail_elems, q;
+  int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
+          // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan)
 };
+
+bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
+
+// LL plan for a one-round message of ng granules: C CTAs per CTA group and
+// chunk size; false if the LL protocol does not apply or does not fit.
+bool ll_plan(lane_comm_t c, int64_t ng, Plan* pl) {
+  if (c->P == 1 || c->ll_bytes == 0 || c->proto == 2 || ng > c->ll_max) return false;
+  if (c->proto == 0 && ng > c->ll_thresh) return false;
+  const int ranks_here = c->emulated ? c->P : 1;
+  int budget = c->ll_ctas > 0 ? c->ll_ctas : (c->emulated ? c->ll_coresident : c->sm_count);
+  if (budget > c->ll_coresident) budget = c->ll_coresident;
+  int C = budget / (ranks_here * c->k);
+  if (C < 1) C = 1;
+  if ((int64_t)C * c->k * ranks_here > c->ll_coresident) return false;  // every CTA must be resident
+  const int64_t slice0 = (ng + c->k - 1) / c->k;
+  int64_t cg = (slice0 + C - 1) / C;
+  if (cg < c->ll_cg_min) cg = c->ll_cg_min;
+  const int64_t nch = lane::n_chunks(slice0, cg);
+  if (nch < C) C = (int)(nch > 0 ? nch : 1);
+  const int64_t cap = lane::round_chunks(ng, c->k, cg);
+  const int64_t sg = lane::ceil_div(cg, c->G), su = lane::ceil_div(sg, c->N);
+  if (cap * sg > c->ll_slot_g || cap * su > c->ll_slot_u) return false;
+  pl->C = C;
+  pl->cg = cg;
+  pl->ll = 1;
+  return true;
+}
 
 int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   const int isz = itemsize_of(dtype);
@@ -285,6 +383,13 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   pl->tail_elems = (int)(count - (uint64_t)(pl->ng - 1) * pl->q);
   pl->round_len0 = pl->ng < c->round_cap ? pl->ng : c->round_cap;
   pl->rounds = (int)((pl->ng + c->round_cap - 1) / c->round_cap);
+  pl->ll = 0;
+  if (c->phase2_ring && c->P > 1) {  // the lane method with a ring inter-node stage: LL rounds only
+    if (!ring_plan(c, pl->ng, true, pl))
+      return fail(c, LANE_ERR_INVALID_ARG, "LANE_PHASE2=ring: CTA capacity or LL inboxes exceeded");
+    return LANE_OK;
+  }
+  if (pl->rounds == 1 && ll_plan(c, pl->ng, pl)) return LANE_OK;
   // CTAs per CTA group: fill the device with all ranks' groups (emulated) or
   // default to 64 CTAs per GPU across the k groups (multi-GPU); env override.
   int ranks_here = c->emulated ? c->P : 1;
@@ -332,7 +437,82 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   return p;
 }
 
+// Plan of the ring algorithms on the LL protocol (flat ring, Alg. 1; lane
+// method with a ring inter-node stage): rounds of at most ll_max granules
+// (one launch each), each split into the comm's k slices and pipeline chunks
+// of a FIXED ring_cg granules — the ring order of an element depends on its
+// chunk (R#21), so the chunking must not depend on the launch configuration.
+// C = CTAs per CTA group (every CTA resident). false: does not fit.
+bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
+  if (c->ll_bytes == 0) return false;
+  const int ranks_here = c->emulated ? c->P : 1;
+  int budget = c->ll_ctas > 0 ? c->ll_ctas : (c->emulated ? c->ll_coresident : c->sm_count);
+  if (budget > c->ll_coresident) budget = c->ll_coresident;
+  int C = budget / (ranks_here * c->k);
+  if (C < 1) C = 1;
+  if ((int64_t)C * c->k * ranks_here > c->ll_coresident) return false;
+  const int64_t RC = c->ll_max, cg = c->ring_cg;
+  const int64_t r0 = ng < RC ? ng : RC;
+  const int64_t nch = lane::n_chunks(lane::ceil_div(r0, c->k), cg);
+  if (nch < C) C = (int)(nch > 0 ? nch : 1);
+  const int64_t cap = lane::round_chunks(r0, c->k, cg);  // the first round is the largest
+  if (lane_ring) {
+    const int64_t sg = lane::ceil_div(cg, c->G), su = lane::ceil_div(sg, c->N);
+    if (cap * sg > c->ll_slot_g || cap * su > c->ll_slot_u) return false;
+  } else if (cap * lane::ceil_div(cg, c->P) > c->ring_slot) {
+    return false;
+  }
+  pl->C = C;
+  pl->cg = cg;
+  pl->rounds = (int)lane::ceil_div(ng, RC);
+  pl->round_len0 = r0;
+  pl->ll = lane_ring ? 2 : 3;
+  return true;
+}
+
+// Launch the rounds of a ring_plan: lane_ring_ll_kernel (flat ring, ll == 3)
+// or lane_ll_kernel with the ring inter-node stage (ll == 2).
+int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
+  const int ranks_here = c->emulated ? c->P : 1;
+  const bool flat = pl.ll == 3;
+  const int64_t RC = c->ll_max;
+  p.ll_slot_g = flat ? c->ring_slot : c->ll_slot_g;
+  p.ll_slot_u = flat ? 0 : c->ll_slot_u;
+  p.ll_set = c->ll_set;
+  p.ring2 = flat ? 0 : 1;
+  p.handshake = 0;
+  p.direct = 0;
+  p.C = pl.C;
+  p.cg = pl.cg;
+  p.sg = lane::ceil_div(pl.cg, flat ? c->P : c->G);
+  p.su = flat ? 0 : lane::ceil_div(p.sg, c->N);
+  c->trace_ctas = 0;
+  for (int r = 0; r < pl.rounds; ++r) {
+    p.round_g0 = (int64_t)r * RC;
+    const int64_t rest = pl.ng - p.round_g0;
+    p.round_len = rest < RC ? rest : RC;
+    p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
+    p.epoch = ++c->epoch;
+    void* args[] = {&p};
+    const void* fn;
+    if (flat)
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ring_ll_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ring_ll_kernel<1>
+                                   : (const void*)lane::ll::lane_ring_ll_kernel<2>;
+    else
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ll_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1>
+                                   : (const void*)lane::ll::lane_ll_kernel<2>;
+    const dim3 grid((unsigned)(ranks_here * c->k * pl.C));
+    cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
+                                : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
+    if (e != cudaSuccess) return cuda_fail(c, e, flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch");
+  }
+  return LANE_OK;
+}
+
 int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
+  if (pl.ll >= 2) return ll_ring_rounds(c, p, pl, dtype, s);
   const int nlocal = p.nlocal;
   for (int r = 0; r < pl.rounds; ++r) {
     p.round_g0 = (int64_t)r * c->round_cap;
@@ -343,13 +523,31 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
+    if (pl.ll) {  // LL protocol: one launch, no scratch flags, no handshake
+      p.ll_slot_g = c->ll_slot_g;
+      p.ll_slot_u = c->ll_slot_u;
+      p.ll_set = c->ll_set;
+      p.handshake = 0;
+      p.direct = 0;
+      c->trace_ctas = (int)grid.x;
+      void* args[] = {&p};
+      const void* fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ll_kernel<0>
+                       : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1>
+                                               : (const void*)lane::ll::lane_ll_kernel<2>;
+      cudaError_t e = c->emulated
+                          ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
+                          : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
+      if (e != cudaSuccess) return cuda_fail(c, e, "lane_ll_kernel launch");
+      continue;
+    }
     c->trace_ctas = (int)grid.x;
     dim3 block((unsigned)(tma ? lane::tma::kThreads : c->threads));
     const size_t smem = tma ? (size_t)lane::tma::kSmemBytes : 0;
     cudaError_t e;
     void* args[] = {&p};
     const void* fn;
-    if (tma && c->lsu_store)
+    const bool lsu_store = c->store_mode == 1 || (c->store_mode == 0 && pl.ng < c->bulk_min);
+    if (tma && lsu_store)
       fn = dtype == LANE_INT32     ? (const void*)lane::tma::lane_tma_kernel<0, true>
            : dtype == LANE_FLOAT32 ? (const void*)lane::tma::lane_tma_kernel<1, true>
                                    : (const void*)lane::tma::lane_tma_kernel<2, true>;
@@ -633,6 +831,63 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   return launch_rounds(c, p, pl, dtype, s);
 }
 
+static int ring_rounds(lane_comm_t c, LaneParams& p, const Plan& lane_pl, int dtype, cudaStream_t s) {
+  if (c->ll_bytes == 0) return fail(c, LANE_ERR_INVALID_ARG, "ring: LANE_LL_MAX_BYTES is 0 (no LL inboxes)");
+  Plan pl = lane_pl;
+  if (!ring_plan(c, lane_pl.ng, false, &pl))
+    return fail(c, LANE_ERR_INVALID_ARG, "ring: procs_per_gpu exceeds the co-resident CTA capacity or inboxes");
+  return ll_ring_rounds(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_ring(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t count, lane_dtype_t dtype,
+                        lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_ring: use lane_allreduce_ring_emulated");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  st = check_buffers(c, sendbuf, recvbuf, bytes, "lane_allreduce_ring");
+  if (st != LANE_OK) return st;
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = c->rank;
+  p.nlocal = 1;
+  p.rk[c->rank].send = static_cast<const char*>(sendbuf);
+  p.rk[c->rank].recv = static_cast<char*>(recvbuf);
+  return ring_rounds(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_ring_emulated(lane_comm_t c, const void* const* sendbufs, void* const* recvbufs, size_t count,
+                                 lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (!c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_ring_emulated: comm is not emulated");
+  if (!sendbufs || !recvbufs) return fail(c, LANE_ERR_INVALID_ARG, "sendbufs/recvbufs: null");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  for (int r = 0; r < c->P; ++r) {
+    st = check_buffers(c, sendbufs[r], recvbufs[r], bytes, ("rank " + std::to_string(r)).c_str());
+    if (st != LANE_OK) return st;
+  }
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = 0;
+  p.nlocal = c->P;
+  for (int r = 0; r < c->P; ++r) {
+    p.rk[r].send = static_cast<const char*>(sendbufs[r]);
+    p.rk[r].recv = static_cast<char*>(recvbufs[r]);
+  }
+  return ring_rounds(c, p, pl, dtype, s);
+}
+
 // Pipelined host-buffer allreduce: the message is cut into granule-aligned
 // pieces (each its own collective allreduce — results do not depend on the
 // partition); piece i+1's H2D copy and piece i-1's D2H copy run on library
@@ -862,9 +1117,38 @@ int lane_allreduce_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, int64_t
   int st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   if (chunk_granules) *chunk_granules = pl.cg;
-  if (round_granules) *round_granules = c->round_cap;
+  if (round_granules) *round_granules = pl.ll >= 2 ? c->ll_max : c->round_cap;
   if (ctas_per_group) *ctas_per_group = pl.C;
   if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
+  return LANE_OK;
+}
+
+int lane_allreduce_ring_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, int64_t* chunk_granules,
+                             int64_t* round_granules, int* ctas_per_group, int* launches) {
+  if (!c) return LANE_ERR_INVALID_ARG;
+  if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
+    return fail(c, LANE_ERR_UNSUPPORTED, "dtype: unsupported lane_dtype_t");
+  const int q = 16 / itemsize_of(dtype);
+  Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  pl.ng = (int64_t)((count + q - 1) / q);
+  if (!ring_plan(c, pl.ng, false, &pl))
+    return fail(c, LANE_ERR_INVALID_ARG, "ring: procs_per_gpu exceeds the co-resident CTA capacity or inboxes");
+  if (chunk_granules) *chunk_granules = pl.cg;
+  if (round_granules) *round_granules = c->ll_max;
+  if (ctas_per_group) *ctas_per_group = pl.C;
+  if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
+  return LANE_OK;
+}
+
+int lane_allreduce_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int* protocol) {
+  if (!c || !protocol) return fail(c, LANE_ERR_INVALID_ARG, "protocol: null argument");
+  if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
+    return fail(c, LANE_ERR_UNSUPPORTED, "dtype: unsupported lane_dtype_t");
+  Plan pl;
+  int st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE);
   return LANE_OK;
 }
 

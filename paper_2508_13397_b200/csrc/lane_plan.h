@@ -66,6 +66,7 @@ struct RankMem {
   char* s2;          // phase-2 inbox: N slots x cap chunks x SU granules
   char* r;           // lane result R: cap chunks x SG granules
   uint32_t* flags;   // F1[G][cap] F2[N][cap] F3[N][cap] F4[G][cap]
+  char* ll;          // low-latency (LL) inboxes: 2 parity sets, see lane_ll.cuh
   const char* send;  // user buffers (only for ranks this launch executes)
   char* recv;
 };
@@ -90,6 +91,10 @@ struct LaneParams {
   uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
   uint32_t* abort_flag; // device word: set when any wait of this comm timed out
   uint64_t* trace;      // optional per-CTA stall accounting (LANE_TRACE=1), else null
+  int64_t ll_slot_g;    // LL protocol: granules per group-part slot (L1, L4), per set
+  int64_t ll_slot_u;    // LL protocol: granules per sub-part slot (L2, L3), per set
+  int64_t ll_set;       // LL protocol: granules per parity set (both kernels agree)
+  int ring2;            // LL lane kernel: 1 = ring inter-node stage (LANE_PHASE2=ring)
 };
 
 // Trace record layout (kTraceWords uint64 per CTA, nanoseconds unless noted).

@@ -444,16 +444,16 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       }
       __threadfence_block();  // acquire the record
       const uint64_t tw = tr ? globaltimer_ns() : 0;
-      __threadfence_system();
+      fence_acq_rel_sys();  // one fence releases every flag of every ready record
       while (head != tail) {
         const RelRec& r = rel_rec[head % kRelSlots];
-        for (int i = 0; i < r.n; ++i) st_release_sys(r.f[i], p.epoch);
+        for (int i = 0; i < r.n; ++i) st_relaxed_sys(r.f[i], p.epoch);
         ++head;
       }
       ring->head = head;
       if (tr) tr_fence += globaltimer_ns() - tw;
     }
-    __threadfence_system();  // every store this CTA made is visible system-wide
+    fence_acq_rel_sys();  // every store this CTA made is visible system-wide
     if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = tr_fence;
     if (p.handshake) {
       // end of call (registered user buffers): the last CTA of this rank tells
@@ -465,8 +465,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
       if ((int)old + 1 == per_rank) {
         atomicExch(cnt, 0u);
+        fence_acq_rel_sys();
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_release_sys(p.rk[q].flags + p.ctl + p.P + x.rank, p.epoch);
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + p.P + x.rank, p.epoch);
         for (int q = 0; q < p.P; ++q)
           if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + p.P + q)) break;
       }
@@ -505,9 +506,11 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
     if (p.handshake) {
       // start of call (registered user buffers): a peer's sendbuf is final and
       // its recvbuf free once its kernel has started (stream order)
-      if (blockIdx.x % per_rank == 0)
+      if (blockIdx.x % per_rank == 0) {
+        fence_acq_rel_sys();
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_release_sys(p.rk[q].flags + p.ctl + x.rank, p.epoch);
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + x.rank, p.epoch);
+      }
       for (int q = 0; q < p.P && ok; ++q)
         if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + q)) ok = false;
       if (ok) fence_async_global();
@@ -742,8 +745,8 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
           mbar_arrive(&empty[s]);
           freed = k;
           fence_async_global();
-          __threadfence_system();
-          for (int r = 0; r < nrel; ++r) st_release_sys(rel[r], p.epoch);
+          fence_acq_rel_sys();
+          for (int r = 0; r < nrel; ++r) st_relaxed_sys(rel[r], p.epoch);
         }
       }
     }

@@ -48,8 +48,13 @@ def main():
     failures = 0
     t0 = time.time()
     maxb = max(counts) * 4
-    for N, G in layouts(P):
-        for k in ks:
+    for N, G, k, proto in [(N, G, k, pr) for (N, G) in layouts(P) for k in ks for pr in ("simple", "ll", "ring2")]:
+        if True:
+            os.environ["LANE_PROTO"] = "ll" if proto == "ring2" else proto  # ll: every message that fits
+            if proto == "ring2":  # the lane method with Alg. 1 as its inter-node stage
+                os.environ["LANE_PHASE2"] = "ring"
+            else:
+                os.environ.pop("LANE_PHASE2", None)
             comm = lane.LaneComm(N, G, k, rank=rank, device=local)
             # registered (zero-copy) buffers: one pair per comm, views at offset 0
             rin = torch.empty(maxb, dtype=torch.uint8, device="cuda")
@@ -79,14 +84,46 @@ def main():
                     else:
                         idx = si.sample_indices(n, 4099, [n // 2, n // 3])
                     xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(P)]
-                    ref = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
+                    if proto == "ring2":
+                        if n > (1 << 20) + 3:  # sampled indices: the ring order needs whole chunks; exact int only
+                            if dtype != "int32":
+                                continue
+                            ref = oracle.brute_force_sum(xs, dtype)
+                        else:
+                            pl = comm.plan(n, dtype)
+                            ref = oracle.lane_allreduce(xs, N, G, k, dtype, pl["chunk_granules"],
+                                                        pl["round_granules"], phase2="ring").out[0]
+                    else:
+                        ref = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
                     got = to_numpy(out[torch.from_numpy(idx).cuda()], dtype)
                     if not np.array_equal(bits(got), bits(ref)):
                         bad = np.nonzero(bits(got) != bits(ref))[0]
-                        print(f"rank {rank} FAIL {N}x{G} k={k} {dtype} n={n} inplace={inplace} reg={registered}: "
+                        print(f"rank {rank} FAIL {proto} {N}x{G} k={k} {dtype} n={n} inplace={inplace} "
+                              f"reg={registered}: "
                               f"{len(bad)} mismatches first {idx[bad[:5]]}", flush=True)
                         failures += 1
-            # host-buffer API (pipelined pieces, ragged tail)
+            # ring allreduce (Alg. 1) vs the ring oracle, on the same comm
+            if proto == "ll":
+                for dtype, n in (("float32", 4099), ("bfloat16", (1 << 20) + 3), ("int32", 7)):
+                    tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
+                    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", 5 + n, rank)
+                    out = torch.empty_like(inp)
+                    comm.allreduce_ring(out, inp)
+                    torch.cuda.synchronize()
+                    comm.check()
+                    xs = [si.generate(dtype, "signed", 5 + n, p_, n) for p_ in range(P)]
+                    pl = comm.plan(n, dtype, algorithm="ring")
+                    ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
+                    if not np.array_equal(bits(to_numpy(out, dtype)), bits(ref)):
+                        print(f"rank {rank} FAIL ring {N}x{G} k={k} {dtype} n={n}", flush=True)
+                        failures += 1
+            # host-buffer API (pipelined pieces, ragged tail; each piece is its own
+            # allreduce, so only the direct stage's order is piece-independent)
+            if proto == "ring2":
+                dist.barrier()
+                comm.close()
+                dist.barrier()
+                continue
             os.environ["LANE_HOST_PIECE_BYTES"] = str(1 << 18)
             n = (1 << 20) + 5
             hx = si.generate("float32", "signed", 77 + k, rank, n)

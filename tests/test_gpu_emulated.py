@@ -43,7 +43,9 @@ def _small_rounds():
 
 def emu(N, G, k):
     import paper_2508_13397_b200 as lane
-    key = (N, G, k, os.environ.get("LANE_ROUND_BYTES"), os.environ.get("LANE_CHUNK_BYTES"))
+    key = (N, G, k) + tuple(os.environ.get(v) for v in ("LANE_ROUND_BYTES", "LANE_CHUNK_BYTES", "LANE_PROTO",
+                                                        "LANE_LL_THRESHOLD_BYTES", "LANE_LL_CTAS",
+                                                        "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES"))
     if key not in _COMMS:
         _COMMS[key] = lane.LaneEmulator(N, G, k, device=0)
     return _COMMS[key]
@@ -77,11 +79,16 @@ def test_seeded_fill_device_matches_numpy():
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "0"])
+@pytest.mark.parametrize("mode", ["1", "2", "0", "ll"])
 def test_parity_layouts(N, G, dtype, mode, monkeypatch):
-    """LANE_DIRECT 1 = direct-pull (emulated default), 2 = direct-push (the
-    registered multi-GPU job set), 0 = staged (the unregistered job set)."""
-    monkeypatch.setenv("LANE_DIRECT", mode)
+    """Simple protocol job sets — LANE_DIRECT 1 = direct-pull (emulated
+    default), 2 = direct-push (the registered multi-GPU job set), 0 = staged
+    (the unregistered job set) — and the LL protocol (lane_ll.cuh)."""
+    if mode == "ll":
+        monkeypatch.setenv("LANE_PROTO", "ll")
+    else:
+        monkeypatch.setenv("LANE_PROTO", "simple")
+        monkeypatch.setenv("LANE_DIRECT", mode)
     for k in (1, 2, 4):
         for n in COUNTS:
             xs = si.generate_all(dtype, "signed", 42 + n, N * G, n)
@@ -98,16 +105,41 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "0"])
+@pytest.mark.parametrize("mode", ["1", "2", "0", "ll", "mixed"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
-    monkeypatch.setenv("LANE_DIRECT", mode)
+    """Repeated calls reuse scratch, flags and (LL) the two inbox parity sets;
+    "mixed" alternates the LL and simple protocols between calls."""
+    if mode == "ll":
+        monkeypatch.setenv("LANE_PROTO", "ll")
+    elif mode == "mixed":
+        monkeypatch.setenv("LANE_LL_THRESHOLD_BYTES", str(64 << 10))
+    else:
+        monkeypatch.setenv("LANE_PROTO", "simple")
+        monkeypatch.setenv("LANE_DIRECT", mode)
     N, G, k = 2, 4, 2
-    for it in range(6):
-        n = [5000, 1 << 16, 33, 1 << 20, 4097, 1 << 16][it]
+    for it in range(9):
+        n = [5000, 1 << 16, 33, 1 << 20, 4097, 1 << 16, 9, 70001, 3][it]
         dtype = ["float32", "bfloat16", "int32"][it % 3]
         xs = si.generate_all(dtype, "signed", 100 + it, 8, n)
         got = run(N, G, k, dtype, xs, inplace=bool(it % 2))
         assert_parity(got, xs, N, G, dtype, f"iter {it}")
+    if mode == "mixed":
+        e = emu(N, G, k)
+        assert e.protocol(5000, "float32") == "ll" and e.protocol(1 << 20, "float32") == "simple"
+
+
+@pytest.mark.parametrize("ctas", ["1", "3", "37"])
+def test_ll_cta_counts_and_chunking(ctas, monkeypatch):
+    """LL protocol with few CTAs per rank (several chunks per CTA, phase-major
+    within a CTA) and a message at the LL capacity's edge."""
+    monkeypatch.setenv("LANE_PROTO", "ll")
+    monkeypatch.setenv("LANE_LL_CTAS", str(int(ctas) * 8))
+    for N, G, k in ((2, 4, 1), (4, 2, 2), (8, 1, 3), (1, 8, 1)):
+        for n in (4097, (1 << 19) + 7):
+            xs = si.generate_all("float32", "signed", 5 + n, 8, n)
+            e = emu(N, G, k)
+            assert e.protocol(n, "float32") == "ll"
+            assert_parity(run(N, G, k, "float32", xs), xs, N, G, "float32", f"ll ctas={ctas} {N}x{G} k={k} n={n}")
 
 
 def test_multi_round_and_chunk_sizes():
@@ -228,3 +260,68 @@ def test_full_size_sampled_parity(N, G, k, dtype, n):
     finally:
         if old is not None:
             os.environ["LANE_ROUND_BYTES"] = old
+
+
+def run_ring(N, G, k, dtype, xs, inplace=False):
+    import torch
+    ins = [to_device(x, dtype, "cuda:0") for x in xs]
+    outs = ins if inplace else [torch.full_like(t, 0) for t in ins]
+    if not inplace:
+        for o in outs:
+            o.view(torch.int16 if dtype == "bfloat16" else torch.int32).fill_(-1)
+    emu(N, G, k).allreduce_ring(outs, ins)
+    torch.cuda.synchronize()
+    emu(N, G, k).check()
+    return [to_numpy(o, dtype) for o in outs]
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_ring_parity(P, dtype):
+    """Ring allreduce (Alg. 1, lane_allreduce_ring_emulated) vs the ring oracle,
+    bit-exact: ring order per chunk, one rounding per hop."""
+    for k in (1, 2, 3):
+        for n in COUNTS:
+            xs = si.generate_all(dtype, "signed", 7 + n, P, n)
+            got = run_ring(1, P, k, dtype, xs, inplace=(n % 2 == 1))
+            pl = emu(1, P, k).plan(n, dtype, algorithm="ring")
+            ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
+            for p, o in enumerate(got):
+                assert np.array_equal(bits(o), bits(ref)), f"ring P={P} k={k} n={n} rank {p}"
+
+
+def test_ring_multi_round_and_interleaved_with_lane(monkeypatch):
+    """Ring messages above the LL capacity run in several launches; ring and
+    lane calls share the LL parity sets and the epoch counter."""
+    monkeypatch.setenv("LANE_LL_MAX_BYTES", str(256 << 10))
+    N, G, k = 2, 2, 2
+    for it, n in enumerate([(1 << 18) + 9, 1000, (1 << 16) + 1, 77]):
+        dtype = ["float32", "int32", "bfloat16", "float32"][it]
+        xs = si.generate_all(dtype, "signed", 50 + it, 4, n)
+        got = run_ring(N, G, k, dtype, xs)
+        pl = emu(N, G, k).plan(n, dtype, algorithm="ring")
+        assert pl["launches"] == -(-n * (2 if dtype == "bfloat16" else 4) // (256 << 10))
+        ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
+        assert all(np.array_equal(bits(o), bits(ref)) for o in got), f"ring it={it}"
+        got = run(N, G, k, dtype, xs)
+        assert_parity(got, xs, N, G, dtype, f"lane it={it}")
+
+
+@pytest.mark.parametrize("N,G", [(2, 2), (4, 2), (8, 1), (1, 8), (2, 4), (3, 2), (4, 1)])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_lane_ring_phase2_parity(N, G, dtype, monkeypatch):
+    """LANE_PHASE2=ring: the lane method with Alg. 1 as the inter-node stage
+    (fig:full_mpi_comparison) vs the oracle's ring variant, bit-exact, with
+    small ring chunks and LL rounds so several chunks and launches occur."""
+    monkeypatch.setenv("LANE_PHASE2", "ring")
+    monkeypatch.setenv("LANE_RING_CHUNK_BYTES", str(8 << 10))
+    monkeypatch.setenv("LANE_LL_MAX_BYTES", str(512 << 10))
+    for k in (1, 3):
+        for n in (1, 7, 4099, (1 << 17) + 5):
+            xs = si.generate_all(dtype, "signed", 3 + n, N * G, n)
+            got = run(N, G, k, dtype, xs, inplace=(n == 7))
+            pl = emu(N, G, k).plan(n, dtype)
+            ref = oracle.lane_allreduce(xs, N, G, k, dtype, pl["chunk_granules"], pl["round_granules"],
+                                        phase2="ring").out[0]
+            for p, o in enumerate(got):
+                assert np.array_equal(bits(o), bits(ref)), f"lane-ring {N}x{G} k={k} n={n} rank {p}"

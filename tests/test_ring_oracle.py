@@ -19,11 +19,11 @@ from oracle import lane_oracle as lo
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 
-def _cases():
+def _cases(kind="case "):
     with open(os.path.join(GOLDEN, "ring_order.txt")) as f:
         for line in f:
             line = line.strip()
-            if line.startswith("case "):
+            if line.startswith(kind):
                 yield line
 
 
@@ -97,7 +97,7 @@ def test_ring_ledger_closed_forms(P, k, n):
     assert np.all(r.sent == 2 * (P - 1) * n // P)
     assert np.all(r.recv == 2 * (P - 1) * n // P)
     # chunk c completes on rank c-1 (the last rp of the reduce-scatter loop)
-    for l, D in enumerate(oracle.ring_chunks(n, 4, P, k)):
+    for D in oracle.ring_chunks(n, 4, P, k):
         for c, (s, e) in enumerate(D):
             assert np.all(r.owner[s:e] == (c - 1) % P)
 
@@ -117,3 +117,84 @@ def test_ring_p1_and_empty():
     assert np.array_equal(oracle.ring_allreduce([x], 1, "float32").out[0], x)
     r = oracle.ring_allreduce([np.zeros(0, np.float32)] * 3, 2, "float32")
     assert all(len(o) == 0 for o in r.out)
+
+
+# ------------------------------------------------ lane method, ring inter-node stage
+@pytest.mark.parametrize("line", list(_cases("lanering ")))
+def test_lane_ring_phase2_fixture(line):
+    f = line.split()
+    dtype, N, G, n = f[2], int(f[3]), int(f[4]), int(f[5])
+    kv = dict(x.split("=") for x in f[6:])
+    ins = [_val(v, dtype) for v in kv["inputs"].split(",")]
+    exp = [_val(v, dtype) for v in kv["expect"].split(",")]
+    xs = [np.full(n, v, dtype=lo.STORAGE[dtype]) for v in ins]
+    r = oracle.lane_allreduce(xs, N, G, 1, dtype, phase2="ring")
+    q = 16 // lo.ITEMSIZE[dtype]
+    for p in range(N * G):
+        for gi, e in enumerate(exp):
+            assert np.all(r.out[p][gi * q:(gi + 1) * q] == e), (p, gi)
+
+
+@pytest.mark.parametrize("P", [3, 4, 8])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_lane_ring_phase2_g1_is_alg1(P, dtype):
+    """G = 1: no intra-node stage, one chunk per slice, the group part is the
+    whole slice and its N sub-parts are exactly Alg. 1's chunks — the lane
+    method with a ring inter-node stage IS the flat ring (two independently
+    written simulations)."""
+    xs = si.generate_all(dtype, "signed", 13, P, 5003)
+    for k in (1, 2):
+        a = oracle.lane_allreduce(xs, P, 1, k, dtype, phase2="ring").out[0]
+        b = oracle.ring_allreduce(xs, k, dtype).out[0]
+        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
+
+
+@pytest.mark.parametrize("N,G", [(1, 4), (2, 4), (2, 2), (1, 8)])
+def test_lane_ring_phase2_small_n_equals_direct(N, G):
+    """N <= 2: at most one commutative add in the lane stage."""
+    for dtype in ("float32", "bfloat16"):
+        xs = si.generate_all(dtype, "signed", 21, N * G, 3001)
+        a = oracle.lane_allreduce(xs, N, G, 2, dtype, phase2="ring")
+        b = oracle.lane_allreduce(xs, N, G, 2, dtype)
+        assert np.array_equal(a.out[0].view(np.uint8), b.out[0].view(np.uint8))
+
+
+@pytest.mark.parametrize("N,G", [(4, 2), (8, 1), (3, 2), (4, 1)])
+def test_lane_ring_phase2_exact_bound_and_ledger(N, G):
+    P = N * G
+    n = 16 * 3 * P * 8
+    xs = si.generate_all("int32", "full", 2, P, n)
+    r = oracle.lane_allreduce(xs, N, G, 3, "int32", phase2="ring")
+    for o in r.out:
+        assert np.array_equal(o, oracle.brute_force_sum(xs, "int32"))
+    # same bytes as the direct stage: 2(P-1)/P * n per rank (V5)
+    assert np.all(r.ledger.total_sent() == 2 * (P - 1) * n // P)
+    for dtype in ("float32", "bfloat16"):
+        xs = si.generate_all(dtype, "signed", 4, P, 4099)
+        r = oracle.lane_allreduce(xs, N, G, 1, dtype, phase2="ring")
+        err = np.abs(oracle.to_float64(r.out[0], dtype) - oracle.brute_force_sum(xs, dtype))
+        u = 2.0 ** -24 + (2.0 ** -8 if dtype == "bfloat16" else 0.0)
+        assert np.all(err <= P * u * oracle.abs_sum(xs, dtype) * (1 + 1e-9))
+
+
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_ring_pipeline_chunks_are_independent_rings(dtype):
+    """R#21: with pipeline chunks every chunk is its own Alg. 1 ring — the
+    chunked result equals running the unchunked ring on each chunk's elements
+    (and the unchunked form on a single chunk), so only the chunk hierarchy,
+    not the ring arithmetic, depends on the plan."""
+    P, k, n, cg = 4, 2, 9001, 97
+    q = 4 if dtype == "float32" else 8
+    xs = si.generate_all(dtype, "signed", 17, P, n)
+    full = oracle.ring_allreduce(xs, k, dtype, chunk_granules=cg).out[0]
+    rings = oracle.ring_chunks(n, 16 // q, P, k, chunk_granules=cg)
+    for D in rings:
+        s, e = D[0][0], D[-1][1]
+        if e > s:
+            piece = oracle.ring_allreduce([x[s:e] for x in xs], 1, dtype).out[0]
+            # the piece's own ring chunks match D only when the piece is granule-aligned (always, s % q == 0)
+            assert np.array_equal(piece.view(np.uint8), full[s:e].view(np.uint8))
+    # chunking changes the bits for fp (different ring start per element) but never int results
+    xi = si.generate_all("int32", "full", 3, P, n)
+    assert np.array_equal(oracle.ring_allreduce(xi, k, "int32", chunk_granules=cg).out[0],
+                          oracle.brute_force_sum(xi, "int32"))

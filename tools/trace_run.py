@@ -19,6 +19,20 @@ import paper_2508_13397_b200 as lane  # noqa: E402
 from seeded_inputs import device as sdev  # noqa: E402
 
 
+def summarize_ll(tr, label):
+    """LL kernel trace: words 0..5 = CTA start, last thread's end of phase A..E."""
+    keys = lane.LaneComm.TRACE_FIELDS[:6]
+    rows = [[t[k] for k in keys] for t in tr if t[keys[0]]]
+    t0 = min(r[0] for r in rows)
+    out = [label + f"  (LL protocol, {len(rows)} CTAs; us after the first CTA started)"]
+    out.append(f"  CTA start        min {0:9.2f}  max {(max(r[0] for r in rows) - t0) / 1e3:9.2f}")
+    for i, ph in enumerate("ABCDE", start=1):
+        v = [r[i] for r in rows if r[i]]
+        if v:
+            out.append(f"  end of phase {ph}   min {(min(v) - t0) / 1e3:9.2f}  max {(max(v) - t0) / 1e3:9.2f}")
+    return "\n".join(out)
+
+
 def summarize(tr, label):
     keys = lane.LaneComm.TRACE_FIELDS
     out = [label]
@@ -49,7 +63,8 @@ def main():
         for _ in range(3):
             emu.allreduce(outs, ins)
         torch.cuda.synchronize()
-        print(summarize(emu.trace(), f"emulated {a.layout} k={a.k}"), flush=True)
+        summ = summarize_ll if emu.protocol(n, a.dtype) == "ll" else summarize
+        print(summ(emu.trace(), f"emulated {a.layout} k={a.k}"), flush=True)
         return
     import torch.distributed as dist
     rank, local = int(os.environ["RANK"]), int(os.environ.get("LOCAL_RANK", 0))
@@ -68,7 +83,8 @@ def main():
     e.record()
     torch.cuda.synchronize()
     tr = comm.trace()
-    txt = summarize(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e):.3f} ms")
+    summ = summarize_ll if comm.protocol(n, a.dtype) == "ll" else summarize
+    txt = summ(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e):.3f} ms")
     for r in range(dist.get_world_size()):
         if r == rank:
             print(txt, flush=True)
