@@ -102,6 +102,9 @@ enum TraceField {
   kTrProdTotal = 0, kTrProdFlagWait, kTrProdEmptyWait, kTrProdTiles,
   kTrStoreTotal, kTrStoreFullWait, kTrStoreSync, kTrStoreReadWait, kTrStoreFlush, kTrStoreJobs,
   kTrPhaseA, kTrPhaseB, kTrPhaseC, kTrPhaseD, kTrPhaseE, kTrBytes,
+  kTrStartAbs,   // producer start (absolute globaltimer)
+  kTrEnterWait,  // producer time in the start-of-call handshake
+  kTrEndAbs,     // releaser past the end-of-call barrier (absolute; rank's last CTA only)
   kTraceWords
 };
 

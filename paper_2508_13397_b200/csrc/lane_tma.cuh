@@ -470,6 +470,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
           if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + p.P + x.rank, p.epoch);
         for (int q = 0; q < p.P; ++q)
           if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + p.P + q)) break;
+        if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEndAbs] = globaltimer_ns();
       }
     }
     return;
@@ -514,7 +515,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       for (int q = 0; q < p.P && ok; ++q)
         if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + q)) ok = false;
       if (ok) fence_async_global();
+      if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEnterWait] = globaltimer_ns() - t_start;
     }
+    if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStartAbs] = t_start;
     uint64_t t_idle = 0;
     // jobs[ph] (shared memory): next job of every phase, built once per job
     bool have[5] = {false, false, false, false, false};

@@ -36,7 +36,14 @@ def summarize_ll(tr, label):
 def summarize(tr, label):
     keys = lane.LaneComm.TRACE_FIELDS
     out = [label]
+    st = [t["start_abs"] for t in tr if t["start_abs"]]
+    ends = [t["end_abs"] for t in tr if t["end_abs"]]
+    if st:
+        out.append(f"  CTA start spread {(max(st) - min(st)) / 1e3:9.2f} us; end-of-call barrier passed at "
+                   f"{(max(ends) - min(st)) / 1e3 if ends else float('nan'):9.2f} us after the first CTA start")
     for key in keys:
+        if key in ("start_abs", "end_abs"):
+            continue
         v = [t[key] for t in tr]
         if key in ("prod_tiles", "store_jobs", "bytes_stored"):
             out.append(f"  {key:16s} mean {statistics.mean(v):12.1f}  max {max(v):12.1f}")
@@ -52,6 +59,8 @@ def main():
     ap.add_argument("--mib", type=float, default=1024)
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--emulated", action="store_true")
+    ap.add_argument("--calls", type=int, default=1,
+                    help="back-to-back calls before reading the trace (>1: steady state, no launch skew)")
     a = ap.parse_args()
     N, G = map(int, a.layout.split("x"))
     tdt = getattr(torch, a.dtype)
@@ -79,12 +88,13 @@ def main():
     dist.barrier()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s.record()
-    comm.allreduce(out, inp)
+    for _ in range(a.calls):
+        comm.allreduce(out, inp)
     e.record()
     torch.cuda.synchronize()
     tr = comm.trace()
     summ = summarize_ll if comm.protocol(n, a.dtype) == "ll" else summarize
-    txt = summ(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e):.3f} ms")
+    txt = summ(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e) / a.calls:.4f} ms/call over {a.calls} calls")
     for r in range(dist.get_world_size()):
         if r == rank:
             print(txt, flush=True)
