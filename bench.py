@@ -33,6 +33,9 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 # NCCL is used ONLY for the timed comparator; the required comparator is ring.
 os.environ.setdefault("NCCL_ALGO", "Ring")
+# NCCL's version banner goes to stdout; the contract is ONE JSON line from rank 0
+if os.environ.get("NCCL_DEBUG", "").upper() in ("VERSION", "WARN"):
+    os.environ.pop("NCCL_DEBUG")
 
 METRIC = "allreduce bus GB/s vs msg size at 2/4/8 B200 vs NCCL ring; % of NVLink roofline"
 NVLINK_PEAK = 770.0  # GB/s per direction per GPU, measured peer copy (B200_PROFILING.md)
@@ -364,7 +367,9 @@ def run_single(args):
                                f"launch), k={k}, {dtype}, {S >> 20} MiB per rank (BASELINE configs[1] layout "
                                f"at its largest size)",
                    "layout": f"{N}x{G}", "procs_per_gpu": k, "bytes_per_rank": S, "emulated": True,
-                   "l2": "inputs larger than L2 (8 x 1 GiB)", "plan": plan},
+                   "protocol": emu.protocol(n, dtype),
+                   "l2": (f"inputs larger than L2 ({P} x {S >> 20} MiB)" if P * S > (126 << 20)
+                          else "inputs fit in L2; not flushed"), "plan": plan},
         "algbw": round(S / (ms * 1e-3) / 1e9, 2),
         "verified": ok,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -473,8 +478,9 @@ def run_multi(args):
         "config": {"workload": f"{N}x{G} virtual nodes on {world} B200 (one process per GPU, IPC peers over "
                                f"NVLink 5), k={k}, {dtype}, {S >> 20} MiB per rank",
                    "layout": f"{N}x{G}", "procs_per_gpu": k, "bytes_per_rank": S, "emulated": False,
-                   "registered_buffers": registered,
-                   "l2": "inputs larger than L2 (1 GiB per rank)", "plan": plan},
+                   "registered_buffers": registered, "protocol": comm.protocol(n, dtype),
+                   "l2": (f"inputs larger than L2 ({S >> 20} MiB per rank)" if S > (126 << 20)
+                          else f"inputs ({S >> 20} MiB per rank) fit in L2; not flushed"), "plan": plan},
         "algbw": round(S / (ms_max * 1e-3) / 1e9, 2),
         "verified": ok,
         "roofline": {"bound": "nvlink", "achieved": round(bw, 2), "peak": NVLINK_PEAK, "unit": "GB/s",

@@ -47,7 +47,8 @@ def build(force: bool = False, verbose: bool = False) -> list[str]:
     for t in TARGETS:
         if not force and not _stale(t):
             continue
-        cmd = [NVCC] + COMMON + (["-Xptxas", "-v"] if t["log"] else []) + t["srcs"] + ["-o", t["out"]]
+        extra = os.environ.get("LANE_NVCC_FLAGS", "").split()  # dev experiments (e.g. -DLANE_TMA_STAGE_KB=24)
+        cmd = [NVCC] + COMMON + extra + (["-Xptxas", "-v"] if t["log"] else []) + t["srcs"] + ["-o", t["out"]]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if t["log"]:
             with open(t["log"], "w") as f:

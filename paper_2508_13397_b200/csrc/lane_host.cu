@@ -218,9 +218,10 @@ int occupancy_of(int engine, int threads) {
 
 template <int DT>
 int ll_occupancy_of() {
-  int nb = 0;
+  int nb = 0, nr = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::ll::lane_ll_kernel<DT>, lane::ll::kThreads, 0);
-  return nb;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nr, lane::ll::lane_ring_ll_kernel<DT>, lane::ll::kThreads, 0);
+  return nb < nr ? nb : nr;
 }
 
 thread_local std::string g_init_error;  // errors of init calls that return no comm
@@ -262,7 +263,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->ll_cg_min = env_i64("LANE_LL_MIN_CHUNK_BYTES", 4 << 10) / 16;
   if (c->ll_cg_min < 16) c->ll_cg_min = 16;
   c->ll_ctas = (int)env_i64("LANE_LL_CTAS", 0);
-  c->bulk_min = env_i64("LANE_BULK_MIN_BYTES", 256 << 20) / 16;
+  c->bulk_min = env_i64("LANE_BULK_MIN_BYTES", 16 << 20) / 16;
   c->ring_cg = env_i64("LANE_RING_CHUNK_BYTES", 64 << 10) / 16;
   if (c->ring_cg < c->ll_cg_min) c->ring_cg = c->ll_cg_min;
   {
@@ -434,6 +435,7 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.abort_flag = c->abort_dev;
   p.trace = c->trace;
   p.ctl = c->ctl;
+  p.releasers = (int)env_i64("LANE_RELEASERS", lane::tma::kReleasers);
   return p;
 }
 

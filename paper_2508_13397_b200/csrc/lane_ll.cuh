@@ -93,7 +93,7 @@ __device__ __forceinline__ bool ll_wait(const LaneParams& p, const uint64_t* lin
 template <class O, class LineF>
 __device__ __forceinline__ bool ll_sum(const LaneParams& p, int n, int own, const uint4& own_v, LineF line,
                                        typename O::Acc& acc) {
-  constexpr int B = 4;
+  constexpr int B = 2;
   for (int s0 = 0; s0 < n; s0 += B) {
     uint4 v[B];
     bool hit[B];
@@ -107,10 +107,13 @@ __device__ __forceinline__ bool ll_sum(const LaneParams& p, int n, int own, cons
     for (int u = 0; u < B; ++u) {
       const int s = s0 + u;
       if (s < n) {
-        if (s == own)
+        if (s == own) {
           v[u] = own_v;
-        else if (!hit[u] && !ll_wait_slow(p, line(s), v[u]))
-          return false;
+        } else if (!hit[u]) {
+          uint4 t;  // the slow path's out-parameter; keeps v[] in registers
+          if (!ll_wait_slow(p, line(s), t)) return false;
+          v[u] = t;
+        }
         if (s == 0)
           O::init(acc, v[u]);
         else

@@ -91,6 +91,7 @@ struct LaneParams {
   uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
   uint32_t* abort_flag; // device word: set when any wait of this comm timed out
   uint64_t* trace;      // optional per-CTA stall accounting (LANE_TRACE=1), else null
+  int releasers;        // TMA engine: active releaser warps (LANE_RELEASERS, default all)
   int64_t ll_slot_g;    // LL protocol: granules per group-part slot (L1, L4), per set
   int64_t ll_slot_u;    // LL protocol: granules per sub-part slot (L2, L3), per set
   int64_t ll_set;       // LL protocol: granules per parity set (both kernels agree)

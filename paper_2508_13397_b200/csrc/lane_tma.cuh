@@ -18,11 +18,15 @@
 //                    tiles into the ring with cp.async.bulk (global -> smem,
 //                    completion on the stage's "full" mbarrier). Peer
 //                    addresses are read straight over NVLink by the TMA unit.
-//   warps 1..W     : consumers — reduce the tile's sources in shared memory
-//                    (fp32 accumulate, canonical order, in place into slot 0);
-//   consumer 0     : storer — cp.async.bulk smem -> global (local or peer),
-//                    frees ring stages, and after a job completes
-//                    (wait_group 0) releases its flags with st.release.sys.
+//   warps 1..R     : releasers (lane 0) — take completed jobs' flag lists
+//                    from a shared-memory ring, fence.acq_rel.sys, then
+//                    relaxed .sys flag stores; R fences in flight at once.
+//   warps R+1..    : consumers — reduce the tile's sources from shared memory
+//                    (fp32 accumulate, canonical order) and store 128-bit
+//                    st.global to every destination (or, from
+//                    LANE_BULK_MIN_BYTES, cp.async.bulk smem -> global by
+//                    consumer 0, the storer); the storer hands a finished
+//                    job's flags to the releasers.
 //
 // Schedule: CTA j of CTA group l owns chunks j, j+C, ... of slice l. The
 // producer issues jobs OUT OF ORDER: it takes the next job of any phase whose
@@ -39,17 +43,31 @@
 namespace lane {
 namespace tma {
 
-constexpr int kStages = 4;
-constexpr int kStageBytes = 48 * 1024;
+#ifndef LANE_TMA_STAGES
+#define LANE_TMA_STAGES 4
+#endif
+#ifndef LANE_TMA_STAGE_KB
+#define LANE_TMA_STAGE_KB 48
+#endif
+#ifndef LANE_TMA_MIN_BLOCKS  // CTAs per SM the register budget is sized for
+#define LANE_TMA_MIN_BLOCKS 1
+#endif
+constexpr int kStages = LANE_TMA_STAGES;
+constexpr int kStageBytes = LANE_TMA_STAGE_KB * 1024;
 constexpr int kStageGranules = kStageBytes / 16;
 constexpr int kConsumerWarps = 6;
-constexpr int kThreads = 32 * (2 + kConsumerWarps);  // producer warp, releaser warp, consumers
+// A system-scope fence takes microseconds, and one thread can only wait for
+// one at a time: kReleasers releaser warps (lane 0 each) publish completed
+// jobs concurrently, each with its own fence.
+constexpr int kReleasers = 4;
+constexpr int kThreads = 32 * (1 + kReleasers + kConsumerWarps);  // producer, releasers, consumers
+constexpr int kConsumerTid0 = 32 * (1 + kReleasers);
 constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
 constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
 constexpr int kJobCacheBytes = 5 * 576;  // producer's next job of every phase
 constexpr int kSmemBytes =
-    kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 64 + kJobCacheBytes;
+    kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 256 + kJobCacheBytes;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -335,10 +353,27 @@ struct RelRec {
 static_assert(sizeof(RelRec) <= 136, "RelRec must fit its smem slot");
 
 struct RelRing {
-  volatile int tail;  // records published by the storer
-  volatile int head;  // records retired by the releaser
-  volatile int done;  // storer finished (or aborted)
+  volatile int tail;   // records published by the storer (record t lives in slot t % kRelSlots)
+  int claim;           // next record index a releaser takes (shared-memory atomicAdd)
+  volatile int done;   // storer finished (or aborted)
+  int exited;          // releasers that left their loop
+  unsigned long long fence_ns;  // trace: releasers' time in fences and flag stores
+  volatile int busy[kRelSlots];  // 1 while the slot's record is published and not yet retired
 };
+static_assert(sizeof(RelRing) + 4 <= 256, "RelRing must fit its smem slot");
+
+// Storer side: publish a completed job's flags to the releasers.
+__device__ __forceinline__ void publish_release(RelRing* ring, RelRec* rel_rec, uint32_t* const* rel, int nrel) {
+  const int t = ring->tail;
+  while (ring->busy[t % kRelSlots]) {
+  }
+  RelRec& r = rel_rec[t % kRelSlots];
+  r.n = nrel;
+  for (int i = 0; i < nrel; ++i) r.f[i] = rel[i];
+  __threadfence_block();
+  ring->busy[t % kRelSlots] = 1;
+  ring->tail = t + 1;
+}
 
 // Relaxed poll (no per-poll fence); a fence_acquire_sys() after the last
 // observation completes the acquire pattern.
@@ -381,7 +416,7 @@ __device__ __forceinline__ ChunkGeo chunk_geo(const LaneParams& p, int64_t cb, c
 }
 
 template <int DT, bool kLsuStore>
-__global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_constant__ LaneParams p) {
+__global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel(const __grid_constant__ LaneParams p) {
   using O = Ops<DT>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -389,7 +424,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
   TileDesc* desc = reinterpret_cast<TileDesc*>(empty + kStages);
   RelRec* rel_rec = reinterpret_cast<RelRec*>(desc + kStages);
   RelRing* ring = reinterpret_cast<RelRing*>(rel_rec + kRelSlots);
-  volatile int* abort_s = reinterpret_cast<volatile int*>(ring + 1);
+  volatile int* abort_s = reinterpret_cast<volatile int*>(reinterpret_cast<char*>(ring) + sizeof(RelRing));
   Job* jobs = reinterpret_cast<Job*>(smem + kSmemBytes - kJobCacheBytes);  // producer only
 
   const int per_rank = p.k * p.C;
@@ -420,41 +455,58 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
     }
     *abort_s = 0;
     ring->tail = 0;
-    ring->head = 0;
+    ring->claim = 0;
     ring->done = 0;
+    ring->exited = 0;
+    ring->fence_ns = 0;
+    for (int i = 0; i < kRelSlots; ++i) ring->busy[i] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  if (tid >= 32 && tid < 64) {
-    // ================================================= releaser (one thread)
-    // Publishes job-completion flags. The fence waits until the job's stores
+  if (tid >= 32 && tid < kConsumerTid0) {
+    // ================================================= releasers (lane 0 of warps 1..kReleasers)
+    // Publish job-completion flags. The fence waits until the job's stores
     // (issued by every consumer before the storer's barrier, hence
     // happening-before this thread's acquire of the record) are visible
-    // system-wide; doing it here keeps the consumer pipeline streaming.
-    if (tid != 32) return;
+    // system-wide; doing it here keeps the consumer pipeline streaming, and
+    // several releasers keep several fences in flight.
+    const int nrw = p.releasers < 1 ? 1 : (p.releasers > kReleasers ? kReleasers : p.releasers);
+    if (tid % 32 != 0 || tid / 32 - 1 >= nrw) return;
     const bool tr = p.trace != nullptr;
     uint64_t tr_fence = 0;
-    int head = 0;
     for (;;) {
-      const int tail = ring->tail;
-      if (tail == head) {
-        if (ring->done && ring->tail == head) break;
-        continue;
+      // claim every published, unclaimed record [c0, c1) at once
+      int c0, c1;
+      for (;;) {
+        c0 = *reinterpret_cast<volatile int*>(&ring->claim);
+        c1 = ring->tail;
+        if (c1 > c0) {
+          if (atomicCAS(&ring->claim, c0, c1) == c0) break;
+          continue;
+        }
+        if (ring->done && ring->tail <= *reinterpret_cast<volatile int*>(&ring->claim)) {
+          c0 = c1 = -1;
+          break;
+        }
       }
-      __threadfence_block();  // acquire the record
+      if (c0 < 0) break;
+      __threadfence_block();  // acquire the records
       const uint64_t tw = tr ? globaltimer_ns() : 0;
-      fence_acq_rel_sys();  // one fence releases every flag of every ready record
-      while (head != tail) {
-        const RelRec& r = rel_rec[head % kRelSlots];
+      fence_acq_rel_sys();  // release pattern: one fence, then relaxed .sys flag stores
+      for (int c = c0; c < c1; ++c) {
+        const RelRec& r = rel_rec[c % kRelSlots];
         for (int i = 0; i < r.n; ++i) st_relaxed_sys(r.f[i], p.epoch);
-        ++head;
       }
-      ring->head = head;
+      __threadfence_block();
+      for (int c = c0; c < c1; ++c) ring->busy[c % kRelSlots] = 0;
       if (tr) tr_fence += globaltimer_ns() - tw;
     }
+    if (tr) atomicAdd(&ring->fence_ns, (unsigned long long)tr_fence);
+    if (atomicAdd(&ring->exited, 1) != nrw - 1) return;  // the last releaser finishes the CTA
+    __threadfence_block();
     fence_acq_rel_sys();  // every store this CTA made is visible system-wide
-    if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = tr_fence;
+    if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = ring->fence_ns;
     if (p.handshake) {
       // end of call (registered user buffers): the last CTA of this rank tells
       // every peer "done with your buffers" and waits until every peer is done
@@ -640,7 +692,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
   }
 
   // ================================================ consumers (+ storer)
-  const int ct = tid - 64;
+  const int ct = tid - kConsumerTid0;
   const bool storer = ct == 0;
   const bool tr = storer && p.trace != nullptr;
   uint64_t tr_full = 0, tr_sync = 0, tr_read = 0, tr_flush = 0, tr_ph[5] = {0, 0, 0, 0, 0}, tr_bytes = 0;
@@ -694,16 +746,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
       consumers_sync();  // every consumer has read the stage and issued its stores
       if (tr) tr_sync += globaltimer_ns() - ts;
       if (storer) {
-        if (nrel > 0) {  // job complete: hand its releases to the releaser warp
+        if (nrel > 0) {  // job complete: hand its releases to the releaser warps
           const uint64_t tw = tr ? globaltimer_ns() : 0;
-          const int tail = ring->tail;
-          while (tail - ring->head >= kRelSlots) {
-          }
-          RelRec& r = rel_rec[tail % kRelSlots];
-          r.n = nrel;
-          for (int i = 0; i < nrel; ++i) r.f[i] = d.rel[i];
-          __threadfence_block();
-          ring->tail = tail + 1;
+          publish_release(ring, rel_rec, d.rel, nrel);
           if (tr) tr_flush += globaltimer_ns() - tw;
         }
         mbar_arrive(&empty[s]);
@@ -741,15 +786,14 @@ __global__ void __launch_bounds__(kThreads, 1) lane_tma_kernel(const __grid_cons
           mbar_arrive(&empty[(k - 1) % kStages]);
           freed = k - 1;
         }
-        if (nrel > 0) {  // job complete: make its stores visible, then release
+        if (nrel > 0) {  // job complete: wait for its bulk stores, hand its releases to the releasers
           const uint64_t tw = tr ? globaltimer_ns() : 0;
           bulk_wait_all();
           if (tr) tr_flush += globaltimer_ns() - tw;
           mbar_arrive(&empty[s]);
           freed = k;
-          fence_async_global();
-          fence_acq_rel_sys();
-          for (int r = 0; r < nrel; ++r) st_relaxed_sys(rel[r], p.epoch);
+          fence_async_global();  // the async-proxy (bulk) writes before the generic handoff
+          publish_release(ring, rel_rec, rel, nrel);
         }
       }
     }
