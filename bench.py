@@ -66,6 +66,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ring", action="store_true",
                     help="sweep: also time the library's ring allreduce (Alg. 1, the paper's standard algorithm)")
+    ap.add_argument("--approach2", action="store_true",
+                    help="sweep: also time the paper's draft 'approach 2' (node allreduce + lane allreduce)")
     ap.add_argument("--sweep", default=None,
                     help="multi-GPU: write busbw vs message size (ours and NCCL ring) as JSONL to this file")
     return ap.parse_args()
@@ -610,7 +612,11 @@ def run_sweep(args):
             ms_r = device_time_ms(lambda: comm.allreduce_ring(out, inp), steps, 5, stream, lambda: dist.barrier())
             ok_r = ring_check(out, P, args.k, dtype, n, 42, comm.plan(n, dtype, algorithm="ring"))
             ok = ok and ok_r
-        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0, ms_p, ms_r], dtype=torch.float64)
+        ms_a = 0.0
+        if args.approach2:  # P L296-297; same bits as the lane method
+            ms_a = device_time_ms(lambda: comm.allreduce_approach2(out, inp), steps, 5, stream, lambda: dist.barrier())
+            ok = ok and sample_check([out], N, G, dtype, n, 42, [rank])
+        t = torch.tensor([ms, ms_n, 0.0 if ok else 1.0, ms_p, ms_r, ms_a], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         row = {"layout": f"{N}x{G}", "k": args.k, "dtype": dtype, "bytes": S, "ms": round(t[0].item(), 4),
                "busbw": round(busbw(S, P, t[0].item()), 2), "nccl_ring_ms": round(t[1].item(), 4),
@@ -619,6 +625,8 @@ def run_sweep(args):
         if args.ring:
             row["lane_ring_alg1_busbw"] = round(busbw(S, P, t[4].item()), 2)
             row["lane_ring_alg1_ms"] = round(t[4].item(), 4)
+        if args.approach2:
+            row["approach2_busbw"] = round(busbw(S, P, t[5].item()), 2)
         row["protocol"] = comm.protocol(n, dtype)
         if ppg:
             row["nccl_ring_ppg"] = args.nccl_ppg

@@ -176,6 +176,22 @@ int lane_allreduce_ring_emulated(lane_comm_t comm, const void* const* sendbufs, 
 int lane_allreduce_ring_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype, int64_t* chunk_granules,
                              int64_t* round_granules, int* ctas_per_group, int* launches);
 
+/* --------------------------------------------------- "approach 2" variant
+ * PAPER.md L296-297 (a bullet of the commented-out draft of §3 "Methods":
+ * "Approach 2: allreduce on node + allreduce off node"): a direct allreduce
+ * among the G GPUs of each node (every member ends with the node sum of the
+ * whole buffer), then a direct allreduce of the WHOLE buffer among the N
+ * lane members. Same association and rounding points as lane_allreduce, so
+ * identical results; the traffic is 2(G-1)/G on node plus 2(N-1)/N off node
+ * of the buffer per rank (the lane stage is not divided by G — the reason
+ * the paper's method reduce-scatters first). LL protocol kernel; messages
+ * above $LANE_LL_MAX_BYTES run in several launches. Same argument rules and
+ * errors as lane_allreduce / lane_allreduce_emulated. */
+int lane_allreduce_approach2(lane_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
+                             lane_dtype_t dtype, lane_op_t op, void* stream);
+int lane_allreduce_approach2_emulated(lane_comm_t comm, const void* const* sendbufs, void* const* recvbufs,
+                                      size_t count, lane_dtype_t dtype, lane_op_t op, void* stream);
+
 /* ----------------------------------------------------------------- common */
 
 /* Release scratch, IPC mappings and staging. Collective in multi-GPU mode:

@@ -29,3 +29,4 @@ from .lane_oracle import (  # noqa: F401
     to_float64,
 )
 from .ring_oracle import RingResult, ring_allreduce, ring_chunks  # noqa: F401,E402
+from .approach2_oracle import Approach2Result, approach2_allreduce  # noqa: F401,E402

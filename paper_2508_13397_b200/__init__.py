@@ -191,6 +191,20 @@ class LaneComm(_CommBase):
         _lib.check(code, self._comm)
         return out
 
+    def allreduce_approach2(self, out, inp, op: str = "sum", stream=None):
+        """The paper's draft "approach 2" (node allreduce, then lane allreduce
+        of the whole buffer): same results as ``allreduce``, more traffic."""
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        _check_dev_tensor(inp, self.device, "inp")
+        _check_dev_tensor(out, self.device, "out")
+        if out.numel() != inp.numel() or out.dtype != inp.dtype:
+            raise LaneError(-1, "out: must match inp in numel and dtype")
+        code = _lib.load().lane_allreduce_approach2(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
+                                                    _dtype_code(inp), 0, _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return out
+
     def register(self, t, group=None) -> int:
         """Collective: register CUDA tensor ``t`` for zero-copy allreduce (every
         rank registers its own buffer of the same size, in the same order).
@@ -283,6 +297,19 @@ class LaneEmulator(_CommBase):
         code = _lib.load().lane_allreduce_ring_emulated(self._comm, self._ptrs(inps, "inps"),
                                                         self._ptrs(outs, "outs"), n, _dtype_code(inps[0]), 0,
                                                         _stream_handle(stream))
+        _lib.check(code, self._comm)
+        return outs
+
+    def allreduce_approach2(self, outs, inps, op: str = "sum", stream=None):
+        """'Approach 2' (node allreduce, then lane allreduce) of all emulated ranks."""
+        if op != "sum":
+            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+        n = inps[0].numel()
+        if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
+            raise LaneError(-1, "all tensors must have the same numel and dtype")
+        code = _lib.load().lane_allreduce_approach2_emulated(self._comm, self._ptrs(inps, "inps"),
+                                                             self._ptrs(outs, "outs"), n, _dtype_code(inps[0]), 0,
+                                                             _stream_handle(stream))
         _lib.check(code, self._comm)
         return outs
 

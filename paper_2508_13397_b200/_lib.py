@@ -55,6 +55,8 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_emulated_host": (I, [P, PP, PP, SZ, I, I, P]),
         "lane_allreduce_ring": (I, [P, P, P, SZ, I, I, P]),
         "lane_allreduce_ring_emulated": (I, [P, PP, PP, SZ, I, I, P]),
+        "lane_allreduce_approach2": (I, [P, P, P, SZ, I, I, P]),
+        "lane_allreduce_approach2_emulated": (I, [P, PP, PP, SZ, I, I, P]),
         "lane_allreduce_ring_plan": (I, [P, SZ, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
                                          ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_allreduce_finalize": (I, [P]),

@@ -82,6 +82,7 @@ struct lane_comm_s {
   int64_t ll_slot_g = 0, ll_slot_u = 0;
   int64_t ring_slot = 0;     // granules per ring RS/AG slot (Alg. 1 on the LL protocol)
   int64_t ring_cg = 0;       // granules per pipeline chunk of the ring algorithms (fixed, R#21)
+  int64_t a2_slot_v = 0;     // granules per lane slot of "approach 2" (whole-chunk lane parts)
   bool phase2_ring = false;  // LANE_PHASE2=ring: lane method with a ring inter-node stage
   int64_t ll_set = 0;        // granules per LL parity set (max of the lane and ring layouts)
   uint64_t ll_bytes = 0;
@@ -179,12 +180,15 @@ void size_scratch(lane_comm_t c) {
     c->ll_slot_g = lane::ceil_div(M, G) + chunks + k * (lane::ceil_div(cgmax, G) + 1) + 16;
     c->ll_slot_u = lane::ceil_div(M, G * N) + 2 * chunks + k * (lane::ceil_div(cgmax, G * N) + 2) + 16;
     c->ring_slot = lane::ceil_div(M, G * N) + chunks + k * (lane::ceil_div(cgmax, G * N) + 1) + 16;
+    c->a2_slot_v = lane::ceil_div(M, N) + chunks + k * (lane::ceil_div(cgmax, N) + 1) + 16;
     const int64_t lane_set = lane::ll::set_granules((int)G, (int)N, c->ll_slot_g, c->ll_slot_u);
     const int64_t ring_set = lane::ll::ring_set_granules((int)(G * N), c->ring_slot);
+    const int64_t a2_set = lane::ll::a2_set_granules((int)G, (int)N, c->ll_slot_g, c->a2_slot_v);
     c->ll_set = lane_set > ring_set ? lane_set : ring_set;
+    if (a2_set > c->ll_set) c->ll_set = a2_set;
     c->ll_bytes = al((uint64_t)(2 * c->ll_set) * lane::ll::kPacketBytes);
   } else {
-    c->ll_slot_g = c->ll_slot_u = c->ring_slot = c->ll_set = 0;
+    c->ll_slot_g = c->ll_slot_u = c->ring_slot = c->a2_slot_v = c->ll_set = 0;
     c->ll_bytes = 0;
   }
   c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes;
@@ -218,10 +222,12 @@ int occupancy_of(int engine, int threads) {
 
 template <int DT>
 int ll_occupancy_of() {
-  int nb = 0, nr = 0;
+  int nb = 0, nr = 0, na = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::ll::lane_ll_kernel<DT>, lane::ll::kThreads, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nr, lane::ll::lane_ring_ll_kernel<DT>, lane::ll::kThreads, 0);
-  return nb < nr ? nb : nr;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&na, lane::ll::lane_a2_ll_kernel<DT>, lane::ll::kThreads, 0);
+  nb = nb < nr ? nb : nr;
+  return nb < na ? nb : na;
 }
 
 thread_local std::string g_init_error;  // errors of init calls that return no comm
@@ -347,10 +353,12 @@ struct Plan {
   int64_t ng, cg, round_len0;
   int rounds, C, tail_elems, q;
   int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
-          // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan)
+          // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan);
+          // 5: "approach 2" (rounds, a2_plan)
 };
 
 bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
+bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl);
 
 // LL plan for a one-round message of ng granules: C CTAs per CTA group and
 // chunk size; false if the LL protocol does not apply or does not fit.
@@ -472,22 +480,51 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
   return true;
 }
 
+// Plan of "approach 2" (lane_a2_ll_kernel): rounds of at most ll_max
+// granules; the chunk size follows the CTA count (the result does not depend
+// on it: canonical order). false: does not fit.
+bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
+  if (c->ll_bytes == 0) return false;
+  const int ranks_here = c->emulated ? c->P : 1;
+  int budget = c->ll_ctas > 0 ? c->ll_ctas : (c->emulated ? c->ll_coresident : c->sm_count);
+  if (budget > c->ll_coresident) budget = c->ll_coresident;
+  int C = budget / (ranks_here * c->k);
+  if (C < 1) C = 1;
+  if ((int64_t)C * c->k * ranks_here > c->ll_coresident) return false;
+  const int64_t RC = c->ll_max;
+  const int64_t r0 = ng < RC ? ng : RC;
+  const int64_t slice0 = lane::ceil_div(r0, c->k);
+  int64_t cg = lane::ceil_div(slice0, C);
+  if (cg < c->ll_cg_min) cg = c->ll_cg_min;
+  const int64_t nch = lane::n_chunks(slice0, cg);
+  if (nch < C) C = (int)(nch > 0 ? nch : 1);
+  const int64_t cap = lane::round_chunks(r0, c->k, cg);
+  if (cap * lane::ceil_div(cg, c->G) > c->ll_slot_g || cap * lane::ceil_div(cg, c->N) > c->a2_slot_v) return false;
+  pl->C = C;
+  pl->cg = cg;
+  pl->rounds = (int)lane::ceil_div(ng, RC);
+  pl->round_len0 = r0;
+  pl->ll = 5;
+  return true;
+}
+
 // Launch the rounds of a ring_plan: lane_ring_ll_kernel (flat ring, ll == 3)
-// or lane_ll_kernel with the ring inter-node stage (ll == 2).
+// or lane_ll_kernel with the ring inter-node stage (ll == 2); or of an
+// a2_plan (ll == 5).
 int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
   const int ranks_here = c->emulated ? c->P : 1;
-  const bool flat = pl.ll == 3;
+  const bool flat = pl.ll == 3, a2 = pl.ll == 5;
   const int64_t RC = c->ll_max;
   p.ll_slot_g = flat ? c->ring_slot : c->ll_slot_g;
-  p.ll_slot_u = flat ? 0 : c->ll_slot_u;
+  p.ll_slot_u = flat ? 0 : (a2 ? c->a2_slot_v : c->ll_slot_u);
   p.ll_set = c->ll_set;
-  p.ring2 = flat ? 0 : 1;
+  p.ring2 = pl.ll == 2 ? 1 : 0;
   p.handshake = 0;
   p.direct = 0;
   p.C = pl.C;
   p.cg = pl.cg;
   p.sg = lane::ceil_div(pl.cg, flat ? c->P : c->G);
-  p.su = flat ? 0 : lane::ceil_div(p.sg, c->N);
+  p.su = flat ? 0 : (a2 ? lane::ceil_div(pl.cg, c->N) : lane::ceil_div(p.sg, c->N));
   c->trace_ctas = 0;
   for (int r = 0; r < pl.rounds; ++r) {
     p.round_g0 = (int64_t)r * RC;
@@ -497,7 +534,11 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     p.epoch = ++c->epoch;
     void* args[] = {&p};
     const void* fn;
-    if (flat)
+    if (a2)
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_a2_ll_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_a2_ll_kernel<1>
+                                   : (const void*)lane::ll::lane_a2_ll_kernel<2>;
+    else if (flat)
       fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ring_ll_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ring_ll_kernel<1>
                                    : (const void*)lane::ll::lane_ring_ll_kernel<2>;
@@ -508,7 +549,8 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     const dim3 grid((unsigned)(ranks_here * c->k * pl.C));
     cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
                                 : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
-    if (e != cudaSuccess) return cuda_fail(c, e, flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch");
+    if (e != cudaSuccess)
+      return cuda_fail(c, e, a2 ? "lane_a2_ll_kernel launch" : (flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch"));
   }
   return LANE_OK;
 }
@@ -888,6 +930,64 @@ int lane_allreduce_ring_emulated(lane_comm_t c, const void* const* sendbufs, voi
     p.rk[r].recv = static_cast<char*>(recvbufs[r]);
   }
   return ring_rounds(c, p, pl, dtype, s);
+}
+
+// "Approach 2" entry points (same argument rules as lane_allreduce / _emulated).
+static int a2_call(lane_comm_t c, LaneParams& p, const Plan& lane_pl, int dtype, cudaStream_t s) {
+  Plan pl = lane_pl;
+  if (!a2_plan(c, lane_pl.ng, &pl))
+    return fail(c, LANE_ERR_INVALID_ARG, "approach2: procs_per_gpu exceeds the co-resident CTA capacity or inboxes");
+  return ll_ring_rounds(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_approach2(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t count,
+                             lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (c->emulated)
+    return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_approach2: use lane_allreduce_approach2_emulated");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  st = check_buffers(c, sendbuf, recvbuf, bytes, "lane_allreduce_approach2");
+  if (st != LANE_OK) return st;
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = c->rank;
+  p.nlocal = 1;
+  p.rk[c->rank].send = static_cast<const char*>(sendbuf);
+  p.rk[c->rank].recv = static_cast<char*>(recvbuf);
+  return a2_call(c, p, pl, dtype, s);
+}
+
+int lane_allreduce_approach2_emulated(lane_comm_t c, const void* const* sendbufs, void* const* recvbufs,
+                                      size_t count, lane_dtype_t dtype, lane_op_t op, void* stream) {
+  int st = check_call(c, count, dtype, op);
+  if (st != LANE_OK) return st;
+  if (!c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_approach2_emulated: comm is not emulated");
+  if (!sendbufs || !recvbufs) return fail(c, LANE_ERR_INVALID_ARG, "sendbufs/recvbufs: null");
+  if (count == 0) return LANE_OK;
+  const uint64_t bytes = (uint64_t)count * itemsize_of(dtype);
+  for (int r = 0; r < c->P; ++r) {
+    st = check_buffers(c, sendbufs[r], recvbufs[r], bytes, ("rank " + std::to_string(r)).c_str());
+    if (st != LANE_OK) return st;
+  }
+  Plan pl;
+  st = make_plan(c, count, dtype, &pl);
+  if (st != LANE_OK) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
+  LaneParams p = base_params(c, pl);
+  p.rank0 = 0;
+  p.nlocal = c->P;
+  for (int r = 0; r < c->P; ++r) {
+    p.rk[r].send = static_cast<const char*>(sendbufs[r]);
+    p.rk[r].recv = static_cast<char*>(recvbufs[r]);
+  }
+  return a2_call(c, p, pl, dtype, s);
 }
 
 // Pipelined host-buffer allreduce: the message is cut into granule-aligned

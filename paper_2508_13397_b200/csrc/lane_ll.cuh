@@ -43,6 +43,9 @@
 namespace lane {
 namespace ll {
 
+#ifndef LANE_LL_MIN_BLOCKS  // CTAs per SM the register budget is sized for
+#define LANE_LL_MIN_BLOCKS 1
+#endif
 constexpr int kThreads = 512;
 constexpr int kPacketBytes = 32;  // one granule (16 B) + four 32-bit epochs
 
@@ -194,7 +197,7 @@ __device__ __forceinline__ void phase_clock_flush(const LaneParams& p, const Pha
 }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 1) lane_ll_kernel(const __grid_constant__ LaneParams p) {
+__global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(const __grid_constant__ LaneParams p) {
   __shared__ uint64_t clk[8];
   const PhaseClock pc = phase_clock_begin(p, clk);
   using O = Ops<DT>;
@@ -404,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll_kernel(const __grid_const
 LANE_HD int64_t ring_set_granules(int P, int64_t ring_slot) { return 2 * (int64_t)(P - 1) * ring_slot; }
 
 template <int DT>
-__global__ void __launch_bounds__(kThreads, 1) lane_ring_ll_kernel(const __grid_constant__ LaneParams p) {
+__global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ring_ll_kernel(const __grid_constant__ LaneParams p) {
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int r = p.rank0 + (int)(blockIdx.x / per_rank);
@@ -467,6 +470,134 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll_kernel(const __grid_
           if (!ll_wait(p, ag(mine, s, id, i), v)) return;
           store_out(msg, g0 + d.start + i, v);
         }
+      }
+    }
+  }
+}
+
+// ========================================================================
+// "Approach 2" (commented-out draft of §3: "allreduce on
+// node + allreduce off node") on the LL protocol: a direct node allreduce
+// (reduce-scatter of part g, then every member gets every part of the node
+// sum T) followed by a direct lane allreduce of the WHOLE chunk (lane part
+// V_a reduced by (a,g) over b ascending, then gathered). Same association and
+// rounding points as the lane method, so the same bits; 2(G-1)/G on node and
+// 2(N-1)/N off node of the buffer per rank (the lane stage is not divided by G).
+//
+// Inboxes (per parity set): L1[G-1] (node RS, as the lane kernel), T[G] (node
+// sum part h, from every node member incl. self: one thread's B result is
+// another thread's C input, the packet is the hand-off), V2[N] (lane RS) and
+// V3[N] (lane AG), chunk strides sg = ceil(cg/G) and sv = ceil(cg/N).
+LANE_HD int64_t a2_set_granules(int G, int N, int64_t slot_g, int64_t slot_v) {
+  return (int64_t)(2 * G - 1) * slot_g + 2 * (int64_t)N * slot_v;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_a2_ll_kernel(const __grid_constant__ LaneParams p) {
+  using O = Ops<DT>;
+  const int per_rank = p.k * p.C;
+  const int rank = p.rank0 + (int)(blockIdx.x / per_rank);
+  const int l = (int)(blockIdx.x % per_rank) / p.C;
+  const int64_t j = blockIdx.x % p.C;
+  const int G = p.G, N = p.N;
+  const int a = rank / G, g = rank % G;
+  const uint32_t ep = p.epoch;
+  const int tid = threadIdx.x;
+  constexpr int nthr = kThreads;
+
+  Msg msg;
+  msg.send = reinterpret_cast<const uint4*>(p.rk[rank].send);
+  msg.recv = reinterpret_cast<uint4*>(p.rk[rank].recv);
+  msg.partial_g = p.tail_elems < p.q ? p.ng - 1 : -1;
+  msg.partial_bytes = p.tail_elems * (16 / p.q);
+
+  const Span sl = rf_split(p.round_len, p.k, l);
+  const int64_t nc = n_chunks(sl.len, p.cg);
+  const int64_t cb = chunk_base(p.round_len, p.k, l, p.cg);
+  auto geo = [&](int64_t c) {
+    ChunkGeo ch;
+    ch.id = cb + c;
+    ch.g0 = p.round_g0 + sl.start + c * p.cg;
+    const int64_t rest = sl.len - c * p.cg;
+    ch.len = rest < p.cg ? rest : p.cg;
+    return ch;
+  };
+  const int64_t slot_g = p.ll_slot_g, slot_v = p.ll_slot_u, sg = p.sg, sv = p.su;
+  auto L1 = [&](int r, int s, int64_t c, int64_t i) {
+    return set_base(p, p.rk[r]) + ((int64_t)s * slot_g + c * sg + i) * 4;
+  };
+  auto T = [&](int r, int h, int64_t c, int64_t i) {
+    return set_base(p, p.rk[r]) + ((int64_t)(G - 1 + h) * slot_g + c * sg + i) * 4;
+  };
+  auto V2 = [&](int r, int b, int64_t c, int64_t i) {
+    return set_base(p, p.rk[r]) + ((int64_t)(2 * G - 1) * slot_g + (int64_t)b * slot_v + c * sv + i) * 4;
+  };
+  auto V3 = [&](int r, int b, int64_t c, int64_t i) {
+    return set_base(p, p.rk[r]) + ((int64_t)(2 * G - 1) * slot_g + (int64_t)(N + b) * slot_v + c * sv + i) * 4;
+  };
+  auto slot_of = [&](int h, int dst_g) { return h < dst_g ? h : h - 1; };
+
+  // ---------------- S1 push: node part gd of x -> (a,gd)
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    for (int t = 1; t < G; ++t) {
+      const int gd = (g + t) % G;
+      const Span pd = rf_split(ch.len, G, gd);
+      for (int64_t i = tid; i < pd.len; i += nthr)
+        ll_store(L1(a * G + gd, slot_of(g, gd), ch.id, i), load_x(msg, ch.g0 + pd.start + i), ep);
+    }
+  }
+  // ---------------- S1 reduce (ascending h) + S2: node sum part g -> every node member's T[g]
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    const Span gp = rf_split(ch.len, G, g);
+    for (int64_t i = tid; i < gp.len; i += nthr) {
+      typename O::Acc acc;
+      const uint4 xv = load_x(msg, ch.g0 + gp.start + i);
+      if (!ll_sum<O>(p, G, g, xv, [&](int h) { return L1(rank, slot_of(h, g), ch.id, i); }, acc)) return;
+      const uint4 tv = O::narrow(acc);
+      for (int t = 0; t < G; ++t) ll_store(T(a * G + (g + t) % G, g, ch.id, i), tv, ep);
+    }
+  }
+  // ---------------- S3 push: lane part V_b of the node sum -> (b,g)'s V2[a]
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    const int64_t base = ch.len / G, rem = ch.len % G, big = rem * (base + 1);
+    for (int t = 1; t <= N; ++t) {
+      const int b = (a + t) % N;  // own part last
+      const Span vb = rf_split(ch.len, N, b);
+      for (int64_t i = tid; i < vb.len; i += nthr) {
+        const int64_t pos = vb.start + i;  // granule of the chunk -> its node part h
+        const int h = pos < big ? (int)(pos / (base + 1)) : (int)(rem + (pos - big) / base);
+        const int64_t hs = h < rem ? h * (base + 1) : big + (h - rem) * base;
+        uint4 v;
+        if (!ll_wait(p, T(rank, h, ch.id, pos - hs), v)) return;
+        ll_store(V2(b * G + g, a, ch.id, i), v, ep);
+      }
+    }
+  }
+  // ---------------- S3 reduce (ascending b) -> recvbuf + S4 push to the lane
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    const Span va = rf_split(ch.len, N, a);
+    for (int64_t i = tid; i < va.len; i += nthr) {
+      typename O::Acc acc;
+      if (!ll_sum<O>(p, N, -1, make_uint4(0, 0, 0, 0), [&](int b) { return V2(rank, b, ch.id, i); }, acc)) return;
+      const uint4 f = O::narrow(acc);
+      store_out(msg, ch.g0 + va.start + i, f);
+      for (int t = 1; t < N; ++t) ll_store(V3(((a + t) % N) * G + g, a, ch.id, i), f, ep);
+    }
+  }
+  // ---------------- S4 receive
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    for (int t = 1; t < N; ++t) {
+      const int b = (a + t) % N;
+      const Span vb = rf_split(ch.len, N, b);
+      for (int64_t i = tid; i < vb.len; i += nthr) {
+        uint4 v;
+        if (!ll_wait(p, V3(rank, b, ch.id, i), v)) return;
+        store_out(msg, ch.g0 + vb.start + i, v);
       }
     }
   }

@@ -117,6 +117,20 @@ def main():
                     if not np.array_equal(bits(to_numpy(out, dtype)), bits(ref)):
                         print(f"rank {rank} FAIL ring {N}x{G} k={k} {dtype} n={n}", flush=True)
                         failures += 1
+            # "approach 2" (P L296-297) vs its oracle (= the lane method's bits)
+            if proto == "ll":
+                for dtype, n in (("float32", 4099), ("bfloat16", (1 << 20) + 3)):
+                    tdt = {"float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
+                    inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", 9 + n, rank)
+                    out = torch.empty_like(inp)
+                    comm.allreduce_approach2(out, inp)
+                    torch.cuda.synchronize()
+                    comm.check()
+                    xs = [si.generate(dtype, "signed", 9 + n, p_, n) for p_ in range(P)]
+                    ref = oracle.approach2_allreduce(xs, N, G, k, dtype).out[0]
+                    if not np.array_equal(bits(to_numpy(out, dtype)), bits(ref)):
+                        print(f"rank {rank} FAIL approach2 {N}x{G} k={k} {dtype} n={n}", flush=True)
+                        failures += 1
             # host-buffer API (pipelined pieces, ragged tail; each piece is its own
             # allreduce, so only the direct stage's order is piece-independent)
             if proto == "ring2":

@@ -325,3 +325,24 @@ def test_lane_ring_phase2_parity(N, G, dtype, monkeypatch):
                                         phase2="ring").out[0]
             for p, o in enumerate(got):
                 assert np.array_equal(bits(o), bits(ref)), f"lane-ring {N}x{G} k={k} n={n} rank {p}"
+
+
+@pytest.mark.parametrize("N,G", [(2, 2), (4, 2), (2, 4), (8, 1), (1, 8), (3, 2), (2, 3)])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_approach2_parity(N, G, dtype, monkeypatch):
+    """lane_allreduce_approach2_emulated ("approach 2", P L296-297) vs the
+    approach-2 oracle — whose outputs are the lane method's bits — with small
+    LL rounds so several launches and chunks occur."""
+    import torch
+    monkeypatch.setenv("LANE_LL_MAX_BYTES", str(512 << 10))
+    for k in (1, 3):
+        for n in (1, 7, 4099, (1 << 17) + 5):
+            xs = si.generate_all(dtype, "signed", 11 + n, N * G, n)
+            ins = [to_device(x, dtype, "cuda:0") for x in xs]
+            outs = ins if n == 7 else [torch.full_like(t, 0) for t in ins]
+            emu(N, G, k).allreduce_approach2(outs, ins)
+            torch.cuda.synchronize()
+            emu(N, G, k).check()
+            ref = oracle.approach2_allreduce(xs, N, G, k, dtype).out[0]
+            for p, o in enumerate(outs):
+                assert np.array_equal(bits(to_numpy(o, dtype)), bits(ref)), f"a2 {N}x{G} k={k} n={n} rank {p}"

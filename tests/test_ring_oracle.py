@@ -198,3 +198,33 @@ def test_ring_pipeline_chunks_are_independent_rings(dtype):
     xi = si.generate_all("int32", "full", 3, P, n)
     assert np.array_equal(oracle.ring_allreduce(xi, k, "int32", chunk_granules=cg).out[0],
                           oracle.brute_force_sum(xi, "int32"))
+
+
+# ------------------------------------------------ "approach 2" (P L296-297)
+@pytest.mark.parametrize("N,G", [(2, 4), (4, 2), (1, 8), (8, 1), (3, 2), (2, 2), (1, 1)])
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+def test_approach2_outputs_equal_lane_method(N, G, dtype):
+    """Node sum then lane sum, each in ascending order with one rounding: the
+    same association as the lane method (R#7/R#8), so the outputs are
+    bit-identical; int32 is also the exact sum."""
+    xs = si.generate_all(dtype, "signed", 31, N * G, 4099)
+    a = oracle.approach2_allreduce(xs, N, G, 2, dtype, chunk_granules=97)
+    b = oracle.lane_allreduce(xs, N, G, 2, dtype).out[0]
+    for o in a.out:
+        assert np.array_equal(o.view(np.uint8), b.view(np.uint8))
+    if dtype == "int32":
+        assert np.array_equal(a.out[0], oracle.brute_force_sum(xs, dtype))
+
+
+@pytest.mark.parametrize("N,G", [(2, 4), (4, 2), (1, 4), (4, 1)])
+def test_approach2_ledger_closed_forms(N, G):
+    """Per rank: (G-1)/G*n each way on node, (N-1)/N*n each way off node —
+    every lane carries the whole buffer (vs n/G per lane for the lane method)."""
+    P = N * G
+    n = 4 * 3 * P * 64
+    xs = si.generate_all("int32", "signed", 1, P, n)
+    r = oracle.approach2_allreduce(xs, N, G, 3, "int32")
+    assert np.all(r.sent["node_rs"] == (G - 1) * n // G) and np.all(r.sent["node_ag"] == (G - 1) * n // G)
+    assert np.all(r.sent["lane_rs"] == (N - 1) * n // N) and np.all(r.sent["lane_ag"] == (N - 1) * n // N)
+    lane = oracle.lane_allreduce(xs, N, G, 3, "int32").ledger.total_sent()
+    assert np.all(sum(r.sent.values()) >= lane)

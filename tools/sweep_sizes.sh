@@ -16,6 +16,8 @@ def cell(r):
     s = f"{r['bytes']>>20}M:{r['busbw']:.0f}/{r['nccl_ring_busbw']:.0f}"
     if "lane_ring_alg1_busbw" in r:
         s += f"/{r['lane_ring_alg1_busbw']:.0f}"
+    if "approach2_busbw" in r:
+        s += f"/a{r['approach2_busbw']:.0f}"
     return s + r.get("protocol", "?")[0] + ("" if r["verified"] else "!")
 print(sys.argv[1] or "default", sys.argv[3], " ".join(cell(r) for r in rows) if rows else "NO OUTPUT")
 PY
