@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--mib", type=float, default=1024)
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--emulated", action="store_true")
+    ap.add_argument("--register", action="store_true", help="register the buffers (direct-push job set, as bench.py)")
     ap.add_argument("--calls", type=int, default=1,
                     help="back-to-back calls before reading the trace (>1: steady state, no launch skew)")
     a = ap.parse_args()
@@ -82,6 +83,9 @@ def main():
     comm = lane.LaneComm(N, G, a.k, rank=rank, device=local)
     inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), a.dtype, "signed", 1, rank)
     out = torch.empty_like(inp)
+    if a.register:
+        comm.register(inp)
+        comm.register(out)
     for _ in range(3):
         comm.allreduce(out, inp)
     torch.cuda.synchronize()
