@@ -109,6 +109,15 @@ __device__ __forceinline__ void bulk_wait_read1() {
   asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+// wait until at most `newer` bulk groups are pending (0..2; larger: 2)
+__device__ __forceinline__ void bulk_wait_upto(int64_t newer) {
+  if (newer >= 2)
+    asm volatile("cp.async.bulk.wait_group 2;" ::: "memory");
+  else if (newer == 1)
+    asm volatile("cp.async.bulk.wait_group 1;" ::: "memory");
+  else
+    asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void fence_async_global() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
@@ -699,6 +708,21 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
   uint64_t tr_jobs = 0;
   const uint64_t t_start = tr ? globaltimer_ns() : 0;
   int64_t freed = -1;  // bulk mode: highest tile whose stage was returned to the producer
+  // bulk mode: the last completed job whose release waits for its bulk stores.
+  // It is released once a newer tile's stores are in flight (wait_group with
+  // one newer group pending), or as soon as the storer would otherwise idle:
+  // a held release may be what a peer waits for before it can feed us.
+  int64_t committed = 0;  // bulk groups committed by the storer
+  int pend_n = -1;        // nrel of the held job, -1 = none
+  int64_t pend_g = 0;     // its last group's sequence number
+  uint32_t* pend_f[kMaxSrc];
+  auto flush_pending = [&](int64_t newer) {
+    if (pend_n < 0) return;
+    bulk_wait_upto(newer);
+    fence_async_global();  // the async-proxy (bulk) writes before the generic handoff
+    publish_release(ring, rel_rec, pend_f, pend_n);
+    pend_n = -1;
+  };
   for (int64_t k = 0;; ++k) {
     const int s = (int)(k % kStages);
     const uint32_t par = (uint32_t)((k / kStages) & 1);
@@ -706,6 +730,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     const uint64_t tf = tr ? globaltimer_ns() : 0;
     bool aborted = false;
     while (!mbar_try_wait(&full[s], par)) {
+      if (!kLsuStore && storer && pend_n >= 0) flush_pending(0);  // do not hold a release while idle
       if ((++spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(p.abort_flag)) {
         aborted = true;
         break;
@@ -779,6 +804,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
           if (cnt > 0) bulk_store(dp, stage, (uint32_t)(cnt * 16));
         }
         bulk_commit();
+        ++committed;
         const uint64_t tq = tr ? globaltimer_ns() : 0;
         bulk_wait_read1();  // every store group but this tile's has read its smem
         if (tr) tr_read += globaltimer_ns() - tq;
@@ -786,15 +812,14 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
           mbar_arrive(&empty[(k - 1) % kStages]);
           freed = k - 1;
         }
-        if (nrel > 0) {  // job complete: wait for its bulk stores, hand its releases to the releasers
-          const uint64_t tw = tr ? globaltimer_ns() : 0;
-          bulk_wait_all();
-          if (tr) tr_flush += globaltimer_ns() - tw;
-          mbar_arrive(&empty[s]);
-          freed = k;
-          fence_async_global();  // the async-proxy (bulk) writes before the generic handoff
-          publish_release(ring, rel_rec, rel, nrel);
+        const uint64_t tw = tr ? globaltimer_ns() : 0;
+        flush_pending(committed - pend_g);  // the held job's groups are older than this tile's
+        if (nrel > 0) {  // job complete: hold its release until its bulk stores are done
+          pend_n = nrel;
+          pend_g = committed;
+          for (int r = 0; r < nrel; ++r) pend_f[r] = rel[r];
         }
+        if (tr) tr_flush += globaltimer_ns() - tw;
       }
     }
     if (tr) {
@@ -803,7 +828,10 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       if (nrel) ++tr_jobs;
     }
   }
-  if (!kLsuStore && storer) bulk_wait_all();
+  if (!kLsuStore && storer) {
+    flush_pending(0);
+    bulk_wait_all();
+  }
   if (storer) {
     __threadfence_block();
     ring->done = 1;
@@ -813,7 +841,6 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     Tr[kTrStoreTotal] = globaltimer_ns() - t_start;
     Tr[kTrStoreFullWait] = tr_full;
     Tr[kTrStoreSync] = tr_sync;
-    if (!kLsuStore) Tr[kTrStoreReadWait] = tr_read;
     Tr[kTrStoreFlush] = tr_flush;
     Tr[kTrStoreJobs] = tr_jobs;
     for (int i = 0; i < 5; ++i) Tr[kTrPhaseA + i] = tr_ph[i];

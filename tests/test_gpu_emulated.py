@@ -47,6 +47,8 @@ def emu(N, G, k):
                                                         "LANE_LL_THRESHOLD_BYTES", "LANE_LL_CTAS",
                                                         "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES"))
     if key not in _COMMS:
+        while len(_COMMS) >= 4:  # every emulated comm holds P ranks' scratch: keep a few
+            _COMMS.pop(next(iter(_COMMS))).close()
         _COMMS[key] = lane.LaneEmulator(N, G, k, device=0)
     return _COMMS[key]
 

@@ -1,0 +1,9 @@
+# 4 GPUs: deferred bulk-store release: parity + sweeps
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_emulated.py -x -q > gpurun_out/e19_pytest_emu.txt 2>&1
+timeout 900 python -m pytest tests/test_gpu_multigpu.py -x -q > gpurun_out/e19_pytest_mp.txt 2>&1
+T="timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node=4 --master-addr 127.0.0.1"
+for L in 2x2 4x1; do
+$T --master-port 29911 tools/tune_mid.py --layout $L --mib 8 16 32 64 256 1024 --iters 20 --cfg "" "LANE_BULK_MIN_BYTES=4194304" "LANE_STORE=lsu" >> gpurun_out/e19_tune.txt 2>&1
+done
+timeout 120 python tools/quick_time.py --layout 2x4 --mib 1024 >> gpurun_out/e19_tune.txt 2>&1
