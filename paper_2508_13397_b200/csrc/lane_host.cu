@@ -837,7 +837,8 @@ int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t cou
         p.rk[q].send = S.peer[q] + so;
         p.rk[q].recv = R.peer[q] + ro;
       }
-    p.direct = env_i64("LANE_DIRECT", 2) == 1 ? 1 : 2;  // push flavour by default on real peers
+    const int64_t dm = env_i64("LANE_DIRECT", 2);  // push flavour by default on real peers
+    p.direct = dm == 1 ? 1 : (dm == 3 ? 3 : 2);
     p.handshake = 1;
   }
   return launch_rounds(c, p, pl, dtype, s);
@@ -867,7 +868,7 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   // emulated: every buffer is addressable; pull flavour by default (fewest HBM
   // bytes), LANE_DIRECT=2 runs the push flavour of the multi-GPU path
   p.direct = c->engine == 1 ? (int)env_i64("LANE_DIRECT", 1) : 0;
-  if (p.direct < 0 || p.direct > 2) p.direct = 1;
+  if (p.direct < 0 || p.direct > 3) p.direct = 1;
   for (int r = 0; r < c->P; ++r) {
     p.rk[r].send = static_cast<const char*>(sendbufs[r]);
     p.rk[r].recv = static_cast<char*>(recvbufs[r]);

@@ -164,10 +164,25 @@ struct Ctx {
 //    stores, the faster direction on this fabric): A and B as staged, C stores
 //    the lane result into every lane member's recvbuf, D pushes my completed
 //    part g from my recvbuf into the node peers' recvbufs; no pull phase.
-enum DirectMode { kStaged = 0, kDirectPull = 1, kDirectPush = 2 };
+//  pull-all (registered user buffers; LANE_DIRECT=3): every job reads local or
+//    peer memory and writes only this rank's memory, so a job's release
+//    fence never waits behind stores in flight to other GPUs: B sums the
+//    node's sendbufs into my S2 (slot b = sub-part b), C sums the lane
+//    members' S2 slot a into my recvbuf, D pulls the lane members' results
+//    from their recvbufs, E pulls the node peers' parts from theirs.
+enum DirectMode { kStaged = 0, kDirectPull = 1, kDirectPush = 2, kPullAll = 3 };
 
 __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
   const int dm = x.p->direct;
+  if (dm == kPullAll) {
+    switch (ph) {
+      case 0: return 0;
+      case 1: return x.G > 1 ? x.N : 0;
+      case 2: return 1;
+      case 3: return x.N - 1;
+      default: return x.G - 1;
+    }
+  }
   switch (ph) {
     case 0: return dm == kDirectPull ? 0 : x.G - 1;
     case 1: return x.G == 1 ? (dm == kDirectPull ? 0 : x.N - 1) : x.N;
@@ -196,6 +211,64 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
   J.nwait = 0;
   J.nrel = 0;
   const Span gp = rf_split(ch.len, G, g);
+  if (p.direct == kPullAll) {
+    if (ph == 1) {  // B: node sum (ascending h) of sub-part b of part g -> my S2 slot b
+      const int b = (a + 1 + t) % N;  // own sub-part last
+      const Span up = rf_split(gp.len, N, b);
+      J.len = up.len;
+      J.m0 = ch.g0 + gp.start + up.start;
+      J.nsrc = G;
+      for (int h = 0; h < G; ++h) J.src[h] = (h == g ? x.msg.send : send_of(p.rk[a * G + h])) + J.m0;
+      J.x_mask = (1u << G) - 1;
+      J.dst[0] = s2_slot(p, *x.me, b, ch.id);
+      J.rel[J.nrel++] = p.rk[b * G + g].flags + f2_idx(p, a, ch.id);
+    } else if (ph == 2) {  // C: lane sum (ascending b) of sub-part a -> my recvbuf
+      const Span up = rf_split(gp.len, N, a);
+      J.len = up.len;
+      J.m0 = ch.g0 + gp.start + up.start;
+      J.nsrc = N;
+      for (int b = 0; b < N; ++b) {
+        if (G == 1) {  // a one-GPU node's sum is its sendbuf
+          J.src[b] = (b == a ? x.msg.send : send_of(p.rk[b * G + g])) + J.m0;
+          J.x_mask |= 1u << b;
+        } else {
+          J.src[b] = s2_slot(p, p.rk[b * G + g], a, ch.id);
+          J.wait[J.nwait++] = x.me->flags + f2_idx(p, b, ch.id);
+        }
+      }
+      J.dst[0] = x.msg.recv + J.m0;
+      J.recv_mask = 1;
+      for (int b = 0; b < N; ++b)
+        if (b != a) J.rel[J.nrel++] = p.rk[b * G + g].flags + f3_idx(p, a, ch.id);
+      if (N == 1)  // part g of my recvbuf is complete
+        for (int h = 0; h < G; ++h)
+          if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
+    } else if (ph == 3) {  // D: pull lane member b's result sub-part -> my recvbuf
+      const int b = (a + 1 + t) % N;
+      const Span up = rf_split(gp.len, N, b);
+      J.len = up.len;
+      J.m0 = ch.g0 + gp.start + up.start;
+      J.src[0] = recv_of(p.rk[b * G + g]) + J.m0;
+      J.x_mask = 1;  // a user buffer: its partial last granule is loaded generically
+      J.wait[J.nwait++] = x.me->flags + f3_idx(p, b, ch.id);
+      J.dst[0] = x.msg.recv + J.m0;
+      J.recv_mask = 1;
+      if (t == N - 2)  // part g of my recvbuf complete (C's and every D's stores precede this)
+        for (int h = 0; h < G; ++h)
+          if (h != g) J.rel[J.nrel++] = p.rk[a * G + h].flags + f4_idx(p, g, ch.id);
+    } else {  // E: pull node peer h's part -> my recvbuf
+      const int h = (g + 1 + t) % G;
+      const Span ph_ = rf_split(ch.len, G, h);
+      J.len = ph_.len;
+      J.m0 = ch.g0 + ph_.start;
+      J.src[0] = recv_of(p.rk[a * G + h]) + J.m0;
+      J.x_mask = 1;
+      J.wait[J.nwait++] = x.me->flags + f4_idx(p, h, ch.id);
+      J.dst[0] = x.msg.recv + J.m0;
+      J.recv_mask = 1;
+    }
+    return;
+  }
   if (ph == 0) {  // A (staged): push part gd of my sendbuf into (a,gd)'s S1
     const int gd = (g + 1 + t) % G;
     const Span pd = rf_split(ch.len, G, gd);

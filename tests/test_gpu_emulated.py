@@ -81,10 +81,11 @@ def test_seeded_fill_device_matches_numpy():
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "0", "ll"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll"])
 def test_parity_layouts(N, G, dtype, mode, monkeypatch):
     """Simple protocol job sets — LANE_DIRECT 1 = direct-pull (emulated
-    default), 2 = direct-push (the registered multi-GPU job set), 0 = staged
+    default), 2 = direct-push (the registered multi-GPU job set), 3 = pull-all
+    (registered, every job writes only its own rank's memory), 0 = staged
     (the unregistered job set) — and the LL protocol (lane_ll.cuh)."""
     if mode == "ll":
         monkeypatch.setenv("LANE_PROTO", "ll")
@@ -107,7 +108,7 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "0", "ll", "mixed"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "mixed"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
     """Repeated calls reuse scratch, flags and (LL) the two inbox parity sets;
     "mixed" alternates the LL and simple protocols between calls."""
