@@ -28,3 +28,17 @@ def test_multigpu_parity(P):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert f"mp_worker P={P}: OK" in out, out[-4000:]
+
+
+def test_watchdog_timeout_p2():
+    """A call that a peer never joins ends by the device watchdog
+    (LANE_ERR_TIMEOUT) instead of hanging the GPU (simple and LL protocols)."""
+    if _ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29611",
+           os.path.join(ROOT, "tests", "mp_timeout_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_timeout_worker: OK" in out, out[-4000:]
