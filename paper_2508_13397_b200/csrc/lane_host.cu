@@ -252,7 +252,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->ctas_per_group = (int)env_i64("LANE_CTAS_PER_GROUP", 0);
   c->round_cap = env_i64("LANE_ROUND_BYTES", (int64_t)1 << 30) / 16;
   c->cg_max = env_i64("LANE_CHUNK_BYTES", 1 << 20) / 16;
-  c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 64 << 10) / 16;
+  c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 128 << 10) / 16;
   c->chunks_per_cta = (int)env_i64("LANE_CHUNKS_PER_CTA", 4);
   if (c->chunks_per_cta < 1) c->chunks_per_cta = 1;
   if (c->round_cap < 1024) return fail(c, LANE_ERR_INVALID_ARG, "LANE_ROUND_BYTES must be >= 16 KiB");
