@@ -563,7 +563,8 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     int64_t rest = pl.ng - p.round_g0;
     p.round_len = rest < c->round_cap ? rest : c->round_cap;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
-    if (p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
+    // the simple protocol's flag arrays hold chunk_cap chunks (the LL plan checked its inboxes itself)
+    if (!pl.ll && p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
