@@ -349,3 +349,26 @@ def test_approach2_parity(N, G, dtype, monkeypatch):
             ref = oracle.approach2_allreduce(xs, N, G, k, dtype).out[0]
             for p, o in enumerate(outs):
                 assert np.array_equal(bits(to_numpy(o, dtype)), bits(ref)), f"a2 {N}x{G} k={k} n={n} rank {p}"
+
+
+@pytest.mark.parametrize("N,G", [(2, 2), (4, 2), (1, 8), (8, 1)])
+def test_lsu_engine_parity(N, G, monkeypatch):
+    """LANE_ENGINE=lsu: the first (plain ld/st.global, phase-major) kernel, kept
+    for A/B measurements — same partition, flags and canonical order."""
+    monkeypatch.setenv("LANE_ENGINE", "lsu")
+    monkeypatch.setenv("LANE_PROTO", "simple")
+    import paper_2508_13397_b200 as lane
+    e = lane.LaneEmulator(N, G, 2, device=0)
+    try:
+        import torch
+        for dtype in ("int32", "float32", "bfloat16"):
+            for n in (7, 4099, (1 << 18) + 5):
+                xs = si.generate_all(dtype, "signed", 61 + n, N * G, n)
+                ins = [to_device(x, dtype, "cuda:0") for x in xs]
+                outs = [torch.full_like(t, 0) for t in ins]
+                e.allreduce(outs, ins)
+                torch.cuda.synchronize()
+                e.check()
+                assert_parity([to_numpy(o, dtype) for o in outs], xs, N, G, dtype, f"lsu {N}x{G} {dtype} n={n}")
+    finally:
+        e.close()
