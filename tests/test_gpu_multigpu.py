@@ -42,3 +42,18 @@ def test_watchdog_timeout_p2():
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "mp_timeout_worker: OK" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_stress_back_to_back(P):
+    """1000 back-to-back calls on one comm across the LL / simple / bulk-store
+    thresholds, registered or not, in place or not; every call checked exactly."""
+    if _ngpus() < P:
+        pytest.skip(f"needs {P} GPUs, have {_ngpus()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29620 + P),
+           os.path.join(ROOT, "tests", "mp_stress_worker.py"), "--iters", "1000"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_stress_worker" in out and ": OK" in out, out[-4000:]
