@@ -93,11 +93,11 @@ class _CommBase:
                 "launches": launches.value}
 
     def protocol(self, count: int, dtype: str = "float32") -> str:
-        """'ll' or 'simple': the signalling protocol a call of this size uses."""
+        """'ll', 'll128' or 'simple': the signalling protocol a call of this size uses."""
         pr = ctypes.c_int()
         _lib.check(_lib.load().lane_allreduce_protocol(self._comm, count, DTYPE[dtype], ctypes.byref(pr)),
                    self._comm)
-        return "ll" if pr.value == 1 else "simple"
+        return {1: "ll", 2: "ll128"}.get(pr.value, "simple")
 
     TRACE_FIELDS = ("prod_total", "prod_flag_wait", "prod_empty_wait", "prod_tiles", "store_total",
                     "store_full_wait", "store_sync", "store_read_wait", "store_flush", "store_jobs",

@@ -23,6 +23,7 @@
 #include "../../include/lane_allreduce.h"
 #include "lane_kernels.cuh"
 #include "lane_ll.cuh"
+#include "lane_ll128.cuh"
 #include "lane_tma.cuh"
 #include "lane_plan.h"
 
@@ -73,7 +74,7 @@ struct lane_comm_s {
   int64_t chunk_cap = 0;   // max chunks per round (flag capacity per flag type)
   uint64_t s1_bytes = 0, s2_bytes = 0, r_bytes = 0, flag_bytes = 0, total_bytes = 0;
   // LL protocol (lane_ll.cuh): message capacity, minimum chunk, inbox geometry
-  int proto = 0;             // 0 = auto, 1 = always LL (when it fits), 2 = never LL
+  int proto = 0;             // 0 = auto, 1 = always LL (when it fits), 2 = never LL (simple), 3 = always LL128
   int64_t ll_max = 0;        // granules: largest message the LL inboxes hold
   int64_t ll_thresh = 0;     // granules: auto mode uses LL up to this size
   int64_t ll_cg_min = 0;     // granules
@@ -85,6 +86,12 @@ struct lane_comm_s {
   int64_t a2_slot_v = 0;     // granules per lane slot of "approach 2" (whole-chunk lane parts)
   bool phase2_ring = false;  // LANE_PHASE2=ring: lane method with a ring inter-node stage
   int64_t ll_set = 0;        // granules per LL parity set (max of the lane and ring layouts)
+  // LL128 protocol (lane_ll128.cuh): shares the LL region (one protocol per call)
+  int64_t ll128_max = 0;     // granules: largest message the LL128 inboxes hold
+  int64_t ll128_lo = 0;      // granules: auto mode uses LL128 above this size ...
+  int64_t ll128_hi = 0;      // ... up to this size
+  int64_t ll128_cg_min = 0;  // granules
+  int64_t ll128_set = 0;     // lines (128 B) per LL128 parity set
   uint64_t ll_bytes = 0;
   std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
   std::vector<void*> opened; // IPC-opened peer allocations
@@ -191,6 +198,22 @@ void size_scratch(lane_comm_t c) {
     c->ll_slot_g = c->ll_slot_u = c->ring_slot = c->a2_slot_v = c->ll_set = 0;
     c->ll_bytes = 0;
   }
+  // LL128 set: a call needs 2*G*N*cap*lu lines (lane_ll128.cuh set_lines).
+  // With G*N*su <= CG + G*N and cap*CG <= M + k*CG this is at most
+  // 2*(M + k*CG + cap*G*N)/7 + 2*cap*G*N lines; sized here for k*CG <= M/4
+  // (true whenever a slice spans >= 4 CTAs or CG is the minimum chunk of a
+  // message >= 4*k*CG_min); the plan checks the exact need and otherwise
+  // falls back to another protocol.
+  const int64_t M8 = c->ll128_max;
+  if (M8 > 0) {
+    const int64_t chunks = M8 / c->ll128_cg_min + k + 1;
+    c->ll128_set = 2 * lane::ceil_div(M8 + M8 / 4 + k * c->ll128_cg_min + chunks * G * N, lane::ll128::kLineGranules) +
+                   2 * G * N * chunks + 64;
+    const uint64_t b8 = al((uint64_t)(2 * c->ll128_set) * lane::ll128::kLineBytes);
+    if (b8 > c->ll_bytes) c->ll_bytes = b8;
+  } else {
+    c->ll128_set = 0;
+  }
   c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes;
 }
 
@@ -261,8 +284,20 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->timeout_ns = (uint64_t)env_i64("LANE_TIMEOUT_MS", 20000) * 1000000ull;
   {
     const char* pr = getenv("LANE_PROTO");
-    c->proto = !pr ? 0 : (strcmp(pr, "ll") == 0 ? 1 : (strcmp(pr, "simple") == 0 ? 2 : 0));
+    c->proto = !pr ? 0
+                   : (strcmp(pr, "ll") == 0       ? 1
+                      : strcmp(pr, "simple") == 0 ? 2
+                      : strcmp(pr, "ll128") == 0  ? 3
+                                                  : 0);
   }
+  // auto range from the P = 2 / P = 4 protocol sweeps (profiles/r01_sizes_protocols_ll128.txt):
+  // LL128 ahead of LL above 1 MiB (2 MiB at P = 2), ahead of simple up to 16 MiB
+  c->ll128_max = env_i64("LANE_LL128_MAX_BYTES", 32 << 20) / 16;
+  if (c->ll128_max < 0) c->ll128_max = 0;
+  c->ll128_lo = env_i64("LANE_LL128_MIN_BYTES", (N * G == 2 ? 2 : 1) << 20) / 16;
+  c->ll128_hi = env_i64("LANE_LL128_THRESHOLD_BYTES", 16 << 20) / 16;
+  c->ll128_cg_min = env_i64("LANE_LL128_MIN_CHUNK_BYTES", 16 << 10) / 16;
+  if (c->ll128_cg_min < 64) c->ll128_cg_min = 64;
   c->ll_max = env_i64("LANE_LL_MAX_BYTES", 16 << 20) / 16;
   if (c->ll_max < 0) c->ll_max = 0;
   c->ll_thresh = env_i64("LANE_LL_THRESHOLD_BYTES", 8 << 20) / 16;
@@ -290,6 +325,13 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     int l0 = ll_occupancy_of<0>(), l1 = ll_occupancy_of<1>(), l2 = ll_occupancy_of<2>();
     int lo = l0 < l1 ? l0 : l1;
     lo = lo < l2 ? lo : l2;
+    int m0 = 0, m1 = 0, m2 = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m0, lane::ll128::lane_ll128_kernel<0>, lane::ll128::kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m1, lane::ll128::lane_ll128_kernel<1>, lane::ll128::kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m2, lane::ll128::lane_ll128_kernel<2>, lane::ll128::kThreads, 0);
+    lo = lo < m0 ? lo : m0;
+    lo = lo < m1 ? lo : m1;
+    lo = lo < m2 ? lo : m2;
     c->ll_coresident = (lo < 1 ? 1 : lo) * c->sm_count;
   }
 
@@ -354,15 +396,22 @@ struct Plan {
   int rounds, C, tail_elems, q;
   int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
           // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan);
-          // 5: "approach 2" (rounds, a2_plan)
+          // 4: LL128 lane kernel, one launch; 5: "approach 2" (rounds, a2_plan)
 };
+
+// Plans whose rounds are LL-capacity sized (ll_ring_rounds launches them).
+bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5; }
 
 bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
 bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl);
 
 // LL plan for a one-round message of ng granules: C CTAs per CTA group and
 // chunk size; false if the LL protocol does not apply or does not fit.
+bool ll128_plan(lane_comm_t c, int64_t ng, Plan* pl);
+
 bool ll_plan(lane_comm_t c, int64_t ng, Plan* pl) {
+  if (c->P > 1 && c->proto == 3) return ll128_plan(c, ng, pl);
+  if (c->P > 1 && c->proto == 0 && ng > c->ll128_lo && ng <= c->ll128_hi && ll128_plan(c, ng, pl)) return true;
   if (c->P == 1 || c->ll_bytes == 0 || c->proto == 2 || ng > c->ll_max) return false;
   if (c->proto == 0 && ng > c->ll_thresh) return false;
   const int ranks_here = c->emulated ? c->P : 1;
@@ -382,6 +431,33 @@ bool ll_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   pl->C = C;
   pl->cg = cg;
   pl->ll = 1;
+  return true;
+}
+
+// LL128 plan: as ll_plan, with the LL128 inbox geometry (lines).
+bool ll128_plan(lane_comm_t c, int64_t ng, Plan* pl) {
+  if (c->P == 1 || c->ll128_set == 0 || ng > c->ll128_max) return false;
+  const int ranks_here = c->emulated ? c->P : 1;
+  int budget = c->ll_ctas > 0 ? c->ll_ctas : (c->emulated ? c->ll_coresident : c->sm_count);
+  if (budget > c->ll_coresident) budget = c->ll_coresident;
+  int C = budget / (ranks_here * c->k);
+  if (C < 1) C = 1;
+  if ((int64_t)C * c->k * ranks_here > c->ll_coresident) return false;  // every CTA must be resident
+  const int64_t slice0 = (ng + c->k - 1) / c->k;
+  int64_t cg = (slice0 + C - 1) / C;
+  // k*CG <= M/4 keeps the inbox sizing bound (size_scratch): with fewer than
+  // 4 CTAs per slice, CTAs take several chunks (phase-major)
+  const int64_t cg_cap = c->ll128_max / (4 * c->k);
+  if (cg > cg_cap) cg = cg_cap;
+  if (cg < c->ll128_cg_min) cg = c->ll128_cg_min;
+  const int64_t nch = lane::n_chunks(slice0, cg);
+  if (nch < C) C = (int)(nch > 0 ? nch : 1);
+  const int64_t cap = lane::round_chunks(ng, c->k, cg);
+  const int64_t lu = lane::ll128::lines_of(lane::ceil_div(lane::ceil_div(cg, c->G), c->N));
+  if (lane::ll128::set_lines(c->G, c->N, cap, lu) > c->ll128_set) return false;
+  pl->C = C;
+  pl->cg = cg;
+  pl->ll = 4;
   return true;
 }
 
@@ -556,7 +632,7 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
 }
 
 int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
-  if (pl.ll >= 2) return ll_ring_rounds(c, p, pl, dtype, s);
+  if (ll_rounds(pl)) return ll_ring_rounds(c, p, pl, dtype, s);
   const int nlocal = p.nlocal;
   for (int r = 0; r < pl.rounds; ++r) {
     p.round_g0 = (int64_t)r * c->round_cap;
@@ -568,6 +644,24 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
+    if (pl.ll == 4) {  // LL128 protocol: one launch, no scratch flags, no handshake
+      const int64_t lu = lane::ll128::lines_of(p.su);
+      p.ll_slot_g = p.cap * c->N * lu;
+      p.ll_slot_u = p.cap * lu;
+      p.ll_set = c->ll128_set;
+      p.handshake = 0;
+      p.direct = 0;
+      c->trace_ctas = (int)grid.x;
+      void* args[] = {&p};
+      const void* fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0>
+                       : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1>
+                                               : (const void*)lane::ll128::lane_ll128_kernel<2>;
+      cudaError_t e = c->emulated
+                          ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s)
+                          : cudaLaunchKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s);
+      if (e != cudaSuccess) return cuda_fail(c, e, "lane_ll128_kernel launch");
+      continue;
+    }
     if (pl.ll) {  // LL protocol: one launch, no scratch flags, no handshake
       p.ll_slot_g = c->ll_slot_g;
       p.ll_slot_u = c->ll_slot_u;
@@ -1221,7 +1315,7 @@ int lane_allreduce_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, int64_t
   int st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   if (chunk_granules) *chunk_granules = pl.cg;
-  if (round_granules) *round_granules = pl.ll >= 2 ? c->ll_max : c->round_cap;
+  if (round_granules) *round_granules = ll_rounds(pl) ? c->ll_max : c->round_cap;
   if (ctas_per_group) *ctas_per_group = pl.C;
   if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
   return LANE_OK;
@@ -1252,7 +1346,7 @@ int lane_allreduce_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int
   Plan pl;
   int st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
-  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE);
+  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : (pl.ll == 4 ? LANE_PROTO_LL128 : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE));
   return LANE_OK;
 }
 

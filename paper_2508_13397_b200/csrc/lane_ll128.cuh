@@ -1,0 +1,412 @@
+// lane_ll128.cuh — 128-byte-line low-latency protocol (LL128) kernel of the
+// multi-lane allreduce for mid-size messages (sm_100a).
+//
+// Same method, partition and canonical reduction order as lane_ll.cuh and
+// lane_tma.cuh (Alg. 2: reduce-scatter on comm_group
+// P L243, allreduce on comm_lane P L246, allgather on comm_group P L248; k
+// slices, P L330-349 / L364-373). What differs is the packet: the LL
+// protocol pairs every 32-bit data word with a 32-bit epoch (2x the bytes on
+// NVLink), which caps it near half the link rate; the simple protocol pays a
+// system-scope fence per hop (5-30 us behind streaming remote stores,
+// profiles/r01_fence_micro_p2.txt). Here a packet is one 128-byte line written
+// by 8 consecutive lanes of a warp in ONE 16-byte-per-lane store instruction:
+// lanes 0..6 carry 7 data granules, lane 7 the call's epoch in all four words
+// (7/8 of the bytes are data). The reader loads the line with the same
+// 8-lane pattern, lane 7 compares the epoch, and the 8 lanes agree through a
+// warp shuffle. Correctness rests on the line being written and read as a
+// unit (no tearing inside an aligned 128-byte line across NVLink); the PTX
+// memory model does not state this, so it is an empirical property of the
+// hardware (R#25), checked by the bit-exact stress tests.
+//
+// Inbox layout (per rank, per parity set; units = 128-byte lines):
+// every chunk slot is line-aligned at SUB-PART granularity (lu = ceil(su/7)
+// lines per sub-part), so that every phase — which all iterate over lane
+// sub-parts — reads and writes the same line for the same granule.
+//   L1[s] s < G-1 : part g of a chunk from node peer h, N sub-parts x lu lines
+//   L2[b] b < N   : sub-part a of part g, node sum of (b,g), lu lines
+//   L3[b] b < N   : sub-part b of part g, lane result of (b,g), lu lines
+//   L4[s] s < G-1 : part h from node peer h, N sub-parts x lu lines
+// Phases (A..E) and the parity-set argument are those of lane_ll.cuh.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "lane_kernels.cuh"
+#include "lane_ll.cuh"
+#include "lane_plan.h"
+
+namespace lane {
+namespace ll128 {
+
+constexpr int kThreads = 512;
+constexpr int kWarps = kThreads / 32;
+constexpr int kLineGranules = 7;  // data granules per 128-byte line
+constexpr int kLineBytes = 128;
+constexpr unsigned kFull = 0xffffffffu;
+
+// Lines of a sub-part slot for a chunk whose sub-parts hold at most su granules.
+LANE_HD int64_t lines_of(int64_t su) { return ceil_div(su, kLineGranules); }
+
+// Lines per parity set for a call: (G-1) L1 + (G-1) L4 slots of N*lu lines
+// per chunk, N L2 + N L3 slots of lu lines per chunk.
+LANE_HD int64_t set_lines(int G, int N, int64_t cap, int64_t lu) { return 2 * (int64_t)G * N * cap * lu; }
+
+__device__ __forceinline__ void line_store(uint4* line, int sl, const uint4& v, uint32_t ep) {
+  const uint4 w = sl == 7 ? make_uint4(ep, ep, ep, ep) : v;
+  asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(line + sl), "r"(w.x), "r"(w.y),
+               "r"(w.z), "r"(w.w)
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 line_load(const uint4* line, int sl) {
+  uint4 v;
+  asm volatile("ld.volatile.global.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "l"(line + sl)
+               : "memory");
+  return v;
+}
+
+// Warp-collective (every lane must call it, unconditionally): does the 8-lane
+// group's line carry this call's epoch? Lane 7 of the group holds the flag
+// words; every lane of the group gets the answer.
+__device__ __forceinline__ bool group_ready(const uint4& v, int sl, uint32_t ep) {
+  const bool f = sl == 7 && v.x == ep && v.y == ep && v.z == ep && v.w == ep;
+  return __shfl_sync(kFull, f, (int)(threadIdx.x & 31) | 7);
+}
+
+// Warp-collective wait: groups with `need` reload their line until it carries
+// the epoch; v holds the line's 16 bytes of this lane. false on timeout/abort
+// (warp-uniform).
+__device__ __noinline__ bool wait_line(const LaneParams& p, const uint4* line, int sl, bool need, uint4& v) {
+  const uint64_t t0 = globaltimer_ns();
+  bool got = !need;
+  for (uint32_t it = 1;; ++it) {
+    if (!got) v = line_load(line, sl);
+    const bool r = group_ready(v, sl, p.epoch);
+    got = got || r;
+    if (__all_sync(kFull, got)) return true;
+    if ((it & 255u) == 0) {
+      bool quit = *reinterpret_cast<volatile uint32_t*>(p.abort_flag) != 0;
+      if (!quit && globaltimer_ns() - t0 > p.timeout_ns) {
+        atomicExch(p.abort_flag, 1u);
+        *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_TIMEOUT);
+        __threadfence_system();
+        quit = true;
+      }
+      if (__any_sync(kFull, quit)) return false;
+    }
+  }
+}
+
+#ifndef LANE_LL128_U  // lines per 8-lane group per warp step (loads in flight per lane)
+#define LANE_LL128_U 2
+#endif
+constexpr int U = LANE_LL128_U;
+
+// A warp step's U lines per 8-lane group: flat position, the line's
+// pointer(s), whether the line exists (act) and whether this lane holds a data
+// granule of its span (dv).
+struct Batch {
+  bool act[U], dv[U];
+  int t[U], b[U];
+  int64_t ln[U], i[U];
+};
+
+// Warp-collective: fetch U lines (inactive lines read as zero, never loaded)
+// and wait until every active line carries the epoch.
+__device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U], int sl,
+                                          uint4 (&v)[U]) {
+  bool got[U], all = true;
+#pragma unroll
+  for (int u = 0; u < U; ++u) v[u] = act[u] ? line_load(ptr[u], sl) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const bool r = group_ready(v[u], sl, p.epoch);
+    got[u] = !act[u] || r;
+    all = all && got[u];
+  }
+  if (__all_sync(kFull, all)) return true;
+#pragma unroll
+  for (int u = 0; u < U; ++u)
+    if (!__all_sync(kFull, got[u]))
+      if (!wait_line(p, ptr[u], sl, !got[u], v[u])) return false;
+  return true;
+}
+
+// Line addresses of one rank's inbox (current parity set).
+struct Inbox128 {
+  uint4* base;             // set base (16-byte units)
+  int64_t slot_g, slot_u;  // lines per L1/L4 slot and per L2/L3 slot
+  int64_t lu;              // lines per sub-part
+  int G, N;
+  __device__ __forceinline__ uint4* at(int64_t line) const { return base + line * 8; }
+  __device__ __forceinline__ uint4* l1(int s, int64_t c, int b, int64_t ln) const {
+    return at((int64_t)s * slot_g + (c * N + b) * lu + ln);
+  }
+  __device__ __forceinline__ uint4* l2(int b, int64_t c, int64_t ln) const {
+    return at((int64_t)(G - 1) * slot_g + (int64_t)b * slot_u + c * lu + ln);
+  }
+  __device__ __forceinline__ uint4* l3(int b, int64_t c, int64_t ln) const {
+    return at((int64_t)(G - 1) * slot_g + (int64_t)(N + b) * slot_u + c * lu + ln);
+  }
+  __device__ __forceinline__ uint4* l4(int s, int64_t c, int b, int64_t ln) const {
+    return at((int64_t)(G - 1) * slot_g + (int64_t)(2 * N) * slot_u + (int64_t)s * slot_g + (c * N + b) * lu + ln);
+  }
+};
+
+// p.ll_set = lines per parity set (stride), p.ll_slot_g / ll_slot_u = lines
+// per slot for this call (host: cap * N * lu, cap * lu).
+__device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem& m) {
+  Inbox128 b;
+  b.base = reinterpret_cast<uint4*>(m.ll) + (int64_t)(p.epoch & 1u) * p.ll_set * 8;
+  b.slot_g = p.ll_slot_g;
+  b.slot_u = p.ll_slot_u;
+  b.lu = lines_of(p.su);
+  b.G = p.G;
+  b.N = p.N;
+  return b;
+}
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_constant__ LaneParams p) {
+  __shared__ uint64_t clk[8];
+  const ll::PhaseClock pc = ll::phase_clock_begin(p, clk);
+  using O = Ops<DT>;
+  const int per_rank = p.k * p.C;
+  const int rank = p.rank0 + (int)(blockIdx.x / per_rank);
+  const int l = (int)(blockIdx.x % per_rank) / p.C;
+  const int64_t j = blockIdx.x % p.C;
+  const int G = p.G, N = p.N;
+  const int a = rank / G, g = rank % G;
+  const uint32_t ep = p.epoch;
+  const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 3, sl = threadIdx.x & 7;
+  const int64_t lu = lines_of(p.su);
+  const uint4 z = make_uint4(0, 0, 0, 0);
+
+  Msg msg;
+  msg.send = reinterpret_cast<const uint4*>(p.rk[rank].send);
+  msg.recv = reinterpret_cast<uint4*>(p.rk[rank].recv);
+  msg.partial_g = p.tail_elems < p.q ? p.ng - 1 : -1;
+  msg.partial_bytes = p.tail_elems * (16 / p.q);
+
+  const Span sl_span = rf_split(p.round_len, p.k, l);
+  const int64_t nc = n_chunks(sl_span.len, p.cg);
+  const int64_t cb = chunk_base(p.round_len, p.k, l, p.cg);
+  auto geo = [&](int64_t c) {
+    ChunkGeo ch;
+    ch.id = cb + c;
+    ch.g0 = p.round_g0 + sl_span.start + c * p.cg;
+    const int64_t rest = sl_span.len - c * p.cg;
+    ch.len = rest < p.cg ? rest : p.cg;
+    return ch;
+  };
+  const Inbox128 me = inbox_of(p, p.rk[rank]);
+  auto slot_of = [&](int h, int dst_g) { return h < dst_g ? h : h - 1; };
+
+  // Every phase walks a flat space of lines (t, b, ln) — t the peer step,
+  // b the sub-part, ln the line in it (lu lines per sub-part, the unused
+  // tail lines of shorter sub-parts inactive) — so all warps share the
+  // phase's work; a warp step takes 4*U consecutive positions (U lines per
+  // 8-lane group, positions V0 + 4u + grp). span(t, b) gives the sub-part's
+  // granule span; the loop trip count is warp-uniform.
+  auto walk = [&](int T, int NB, auto span, auto f) -> bool {
+    const int64_t total = (int64_t)T * NB * lu;
+    for (int64_t V0 = (int64_t)warp * 4 * U; V0 < total; V0 += kWarps * 4 * U) {
+      Batch q;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = V0 + 4 * u + grp;
+        q.act[u] = v < total;
+        // positions stay far below 2^31 (total <= M/7 + G*N lines): 32-bit division
+        const uint32_t v32 = q.act[u] ? (uint32_t)v : 0u, lu32 = (uint32_t)lu;
+        const uint32_t r = v32 / lu32;
+        q.ln[u] = v32 - r * lu32;
+        q.b[u] = (int)(r % (uint32_t)NB);
+        q.t[u] = (int)(r / (uint32_t)NB);
+        const Span up = span(q.t[u], q.b[u]);
+        q.act[u] = q.act[u] && q.ln[u] < lines_of(up.len);
+        q.i[u] = q.ln[u] * kLineGranules + sl;
+        q.dv[u] = q.act[u] && sl < kLineGranules && q.i[u] < up.len;
+        q.i[u] += up.start;  // granule of the span's chunk-relative part
+      }
+      if (!f(q)) return false;
+    }
+    return true;
+  };
+
+  // ---------------- A: phase-1 push of the node peers' parts (t = 1..G-1 -> peer gd = g+t)
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    auto span = [&](int t, int b) {
+      const Span pd = rf_split(ch.len, G, (g + 1 + t) % G);
+      Span up = rf_split(pd.len, N, b);
+      up.start += pd.start;  // granule offset within the chunk
+      return up;
+    };
+    walk(G - 1, N, span, [&](const Batch& q) {
+      uint4 x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) x[u] = q.dv[u] ? load_x(msg, ch.g0 + q.i[u]) : z;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q.act[u]) {
+          const int gd = (g + 1 + q.t[u]) % G;
+          line_store(inbox_of(p, p.rk[a * G + gd]).l1(slot_of(g, gd), ch.id, q.b[u], q.ln[u]), sl, x[u], ep);
+        }
+      return true;
+    });
+  }
+  pc.end(1);
+
+  // ---------------- B: phase-1 reduce (ascending h) -> phase-2 reduce-scatter push
+  // (t = 0..N-1 -> sub-part b = a+1+t: remote sub-parts first, own last)
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    const Span gp = rf_split(ch.len, G, g);
+    auto span = [&](int t, int) {
+      Span up = rf_split(gp.len, N, (a + 1 + t) % N);
+      up.start += gp.start;
+      return up;
+    };
+    const bool ok = walk(N, 1, span, [&](const Batch& q) {
+      typename O::Acc acc[U];
+      for (int h = 0; h < G; ++h) {  // warp-uniform, ascending (R#7)
+        uint4 v[U];
+        if (h == g) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) v[u] = q.dv[u] ? load_x(msg, ch.g0 + q.i[u]) : z;
+        } else {
+          const uint4* ptr[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) ptr[u] = me.l1(slot_of(h, g), ch.id, (a + 1 + q.t[u]) % N, q.ln[u]);
+          if (!get_lines(p, ptr, q.act, sl, v)) return false;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (h == 0)
+            O::init(acc[u], v[u]);
+          else
+            O::add(acc[u], v[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q.act[u]) {
+          const int b = (a + 1 + q.t[u]) % N;
+          line_store(inbox_of(p, p.rk[b * G + g]).l2(a, ch.id, q.ln[u]), sl, O::narrow(acc[u]), ep);
+        }
+      return true;
+    });
+    if (!ok) return;
+  }
+  pc.end(2);
+
+  // ---------------- C: phase-2 reduce (ascending b) -> recvbuf + lane AG + phase-3 forward
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    const Span gp = rf_split(ch.len, G, g);
+    auto span = [&](int, int) {
+      Span up = rf_split(gp.len, N, a);
+      up.start += gp.start;
+      return up;
+    };
+    const bool ok = walk(1, 1, span, [&](const Batch& q) {
+      typename O::Acc acc[U];
+      for (int b = 0; b < N; ++b) {  // warp-uniform, ascending (R#7)
+        uint4 v[U];
+        const uint4* ptr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ptr[u] = me.l2(b, ch.id, q.ln[u]);
+        if (!get_lines(p, ptr, q.act, sl, v)) return false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (b == 0)
+            O::init(acc[u], v[u]);
+          else
+            O::add(acc[u], v[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint4 f = O::narrow(acc[u]);
+        if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], f);
+        if (q.act[u]) {
+          for (int t = 1; t < N; ++t) {
+            const int b = (a + t) % N;
+            line_store(inbox_of(p, p.rk[b * G + g]).l3(a, ch.id, q.ln[u]), sl, f, ep);
+          }
+          for (int t = 1; t < G; ++t) {
+            const int h = (g + t) % G;
+            line_store(inbox_of(p, p.rk[a * G + h]).l4(slot_of(g, h), ch.id, a, q.ln[u]), sl, f, ep);
+          }
+        }
+      }
+      return true;
+    });
+    if (!ok) return;
+  }
+  pc.end(3);
+
+  // ---------------- D: phase-2 allgather receive -> recvbuf + phase-3 forward
+  // (t = 0..N-2 -> lane peer b = a+1+t)
+  if (N > 1)
+    for (int64_t c = j; c < nc; c += p.C) {
+      const ChunkGeo ch = geo(c);
+      const Span gp = rf_split(ch.len, G, g);
+      auto span = [&](int t, int) {
+        Span up = rf_split(gp.len, N, (a + 1 + t) % N);
+        up.start += gp.start;
+        return up;
+      };
+      const bool ok = walk(N - 1, 1, span, [&](const Batch& q) {
+        uint4 v[U];
+        const uint4* ptr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) ptr[u] = me.l3((a + 1 + q.t[u]) % N, ch.id, q.ln[u]);
+        if (!get_lines(p, ptr, q.act, sl, v)) return false;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
+          if (q.act[u]) {
+            const int b = (a + 1 + q.t[u]) % N;
+            for (int t2 = 1; t2 < G; ++t2) {
+              const int h = (g + t2) % G;
+              line_store(inbox_of(p, p.rk[a * G + h]).l4(slot_of(g, h), ch.id, b, q.ln[u]), sl, v[u], ep);
+            }
+          }
+        }
+        return true;
+      });
+      if (!ok) return;
+    }
+  pc.end(4);
+
+  // ---------------- E: phase-3 allgather receive (t = 0..G-2 -> node peer h = g+1+t)
+  for (int64_t c = j; c < nc; c += p.C) {
+    const ChunkGeo ch = geo(c);
+    auto span = [&](int t, int b) {
+      const Span ph = rf_split(ch.len, G, (g + 1 + t) % G);
+      Span up = rf_split(ph.len, N, b);
+      up.start += ph.start;
+      return up;
+    };
+    const bool ok = walk(G - 1, N, span, [&](const Batch& q) {
+      uint4 v[U];
+      const uint4* ptr[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) ptr[u] = me.l4(slot_of((g + 1 + q.t[u]) % G, g), ch.id, q.b[u], q.ln[u]);
+      if (!get_lines(p, ptr, q.act, sl, v)) return false;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
+      return true;
+    });
+    if (!ok) return;
+  }
+  pc.end(5);
+  ll::phase_clock_flush(p, pc);
+}
+
+}  // namespace ll128
+}  // namespace lane

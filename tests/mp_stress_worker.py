@@ -1,5 +1,5 @@
 """Stress (multi-GPU): thousands of back-to-back allreduces on one comm,
-alternating the LL and simple protocols, sizes across the LL threshold and
+alternating the LL, LL128 and simple protocols, sizes across their thresholds and
 the bulk-store threshold, registered and unregistered buffers, in-place and
 out-of-place — every call checked exactly (int32: the expected sum is a
 closed form, computed on the device with plain torch ops). Looks for rare
@@ -38,7 +38,8 @@ def main():
     rout = torch.empty_like(rin)
     comm.register(rin)
     comm.register(rout)
-    sizes = [1, 1000, 4099, 1 << 18, (1 << 21) + 3, (2 << 20) + 17, (5 << 20) + 1, nmax]  # LL .. simple+bulk
+    # LL (<= 1 MiB), LL128 (1-16 MiB), simple, simple with bulk stores (>= 16 MiB)
+    sizes = [1, 1000, 4099, 1 << 18, (3 << 18) + 5, (1 << 21) + 3, (1 << 22) - 1, (2 << 20) + 17, (5 << 20) + 1, nmax]
     g = torch.Generator().manual_seed(1234)  # same sequence on every rank
     bad = 0
     t0 = time.time()

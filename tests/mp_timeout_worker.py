@@ -26,7 +26,7 @@ def main():
     dist.init_process_group("gloo")
     os.environ["LANE_TIMEOUT_MS"] = "1500"
     bad = 0
-    for proto, n in (("simple", 1 << 20), ("ll", 4099)):
+    for proto, n in (("simple", 1 << 20), ("ll", 4099), ("ll128", 1 << 20)):
         os.environ["LANE_PROTO"] = proto
         comm = lane.LaneComm(1, world, 1, rank=rank, device=local)
         x = torch.ones(n, device="cuda")

@@ -49,9 +49,10 @@ def main():
     t0 = time.time()
     maxb = max(counts) * 4
     for N, G, k, proto in [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
-                           for pr in ("simple", "pull", "ll", "ring2")]:
+                           for pr in ("simple", "pull", "ll", "ll128", "ring2")]:
         if True:
-            os.environ["LANE_PROTO"] = "simple" if proto in ("simple", "pull") else "ll"  # ll: all that fits
+            # ll / ll128: every call that fits that protocol's inboxes
+            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "ll128": "ll128"}.get(proto, "ll")
             os.environ["LANE_DIRECT"] = "3" if proto == "pull" else "2"  # registered job set: push / pull-all
             if proto == "ring2":  # the lane method with Alg. 1 as its inter-node stage
                 os.environ["LANE_PHASE2"] = "ring"

@@ -45,7 +45,9 @@ def emu(N, G, k):
     import paper_2508_13397_b200 as lane
     key = (N, G, k) + tuple(os.environ.get(v) for v in ("LANE_ROUND_BYTES", "LANE_CHUNK_BYTES", "LANE_PROTO",
                                                         "LANE_LL_THRESHOLD_BYTES", "LANE_LL_CTAS",
-                                                        "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES"))
+                                                        "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES",
+                                                        "LANE_LL128_MIN_BYTES", "LANE_LL128_THRESHOLD_BYTES",
+                                                        "LANE_LL128_MAX_BYTES"))
     if key not in _COMMS:
         while len(_COMMS) >= 4:  # every emulated comm holds P ranks' scratch: keep a few
             _COMMS.pop(next(iter(_COMMS))).close()
@@ -81,19 +83,22 @@ def test_seeded_fill_device_matches_numpy():
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128"])
 def test_parity_layouts(N, G, dtype, mode, monkeypatch):
     """Simple protocol job sets — LANE_DIRECT 1 = direct-pull (emulated
     default), 2 = direct-push (the registered multi-GPU job set), 3 = pull-all
     (registered, every job writes only its own rank's memory), 0 = staged
-    (the unregistered job set) — and the LL protocol (lane_ll.cuh)."""
-    if mode == "ll":
-        monkeypatch.setenv("LANE_PROTO", "ll")
+    (the unregistered job set) — and the LL and LL128 protocols (lane_ll.cuh,
+    lane_ll128.cuh)."""
+    if mode in ("ll", "ll128"):
+        monkeypatch.setenv("LANE_PROTO", mode)
     else:
         monkeypatch.setenv("LANE_PROTO", "simple")
         monkeypatch.setenv("LANE_DIRECT", mode)
     for k in (1, 2, 4):
         for n in COUNTS:
+            if mode in ("ll", "ll128"):
+                assert emu(N, G, k).protocol(n, dtype) == mode
             xs = si.generate_all(dtype, "signed", 42 + n, N * G, n)
             got = run(N, G, k, dtype, xs)
             assert_parity(got, xs, N, G, dtype, f"{N}x{G} k={k} n={n} mode={mode}")
@@ -108,14 +113,16 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "mixed"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "mixed"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
-    """Repeated calls reuse scratch, flags and (LL) the two inbox parity sets;
-    "mixed" alternates the LL and simple protocols between calls."""
-    if mode == "ll":
-        monkeypatch.setenv("LANE_PROTO", "ll")
+    """Repeated calls reuse scratch, flags and (LL, LL128) the two inbox parity
+    sets; "mixed" alternates the LL, LL128 and simple protocols between calls."""
+    if mode in ("ll", "ll128"):
+        monkeypatch.setenv("LANE_PROTO", mode)
     elif mode == "mixed":
         monkeypatch.setenv("LANE_LL_THRESHOLD_BYTES", str(64 << 10))
+        monkeypatch.setenv("LANE_LL128_MIN_BYTES", str(64 << 10))
+        monkeypatch.setenv("LANE_LL128_THRESHOLD_BYTES", str(1 << 20))
     else:
         monkeypatch.setenv("LANE_PROTO", "simple")
         monkeypatch.setenv("LANE_DIRECT", mode)
@@ -128,7 +135,8 @@ def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
         assert_parity(got, xs, N, G, dtype, f"iter {it}")
     if mode == "mixed":
         e = emu(N, G, k)
-        assert e.protocol(5000, "float32") == "ll" and e.protocol(1 << 20, "float32") == "simple"
+        assert e.protocol(5000, "float32") == "ll" and e.protocol(1 << 16, "float32") == "ll128"
+        assert e.protocol(1 << 20, "float32") == "simple"
 
 
 @pytest.mark.parametrize("ctas", ["1", "3", "37"])
@@ -143,6 +151,24 @@ def test_ll_cta_counts_and_chunking(ctas, monkeypatch):
             e = emu(N, G, k)
             assert e.protocol(n, "float32") == "ll"
             assert_parity(run(N, G, k, "float32", xs), xs, N, G, "float32", f"ll ctas={ctas} {N}x{G} k={k} n={n}")
+
+
+@pytest.mark.parametrize("ctas", ["1", "5", "148"])
+def test_ll128_cta_counts_and_sizes(ctas, monkeypatch):
+    """LL128 protocol (lane_ll128.cuh): few CTAs per rank (several chunks per
+    CTA, phase-major within a CTA; more lines per sub-part than a warp step
+    covers), ragged sizes, and a message at the LL128 capacity's edge."""
+    monkeypatch.setenv("LANE_PROTO", "ll128")
+    monkeypatch.setenv("LANE_ROUND_BYTES", str(64 << 20))  # LL protocols run one-round messages only
+    monkeypatch.setenv("LANE_LL_CTAS", str(int(ctas) * 8))
+    monkeypatch.setenv("LANE_LL128_MAX_BYTES", str(16 << 20))
+    for N, G, k in ((2, 4, 1), (4, 2, 2), (8, 1, 3), (1, 8, 1)):
+        for n in (4097, (1 << 19) + 7, (4 << 20) - 3):
+            xs = si.generate_all("float32", "signed", 5 + n, 8, n)
+            e = emu(N, G, k)
+            assert e.protocol(n, "float32") == "ll128"
+            assert_parity(run(N, G, k, "float32", xs), xs, N, G, "float32", f"ll128 ctas={ctas} {N}x{G} k={k} n={n}")
+    assert emu(2, 4, 1).protocol((4 << 20) + 4, "float32") == "simple"  # beyond the LL128 capacity
 
 
 def test_multi_round_and_chunk_sizes():

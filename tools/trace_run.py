@@ -73,7 +73,7 @@ def main():
         for _ in range(3):
             emu.allreduce(outs, ins)
         torch.cuda.synchronize()
-        summ = summarize_ll if emu.protocol(n, a.dtype) == "ll" else summarize
+        summ = summarize_ll if emu.protocol(n, a.dtype) in ("ll", "ll128") else summarize
         print(summ(emu.trace(), f"emulated {a.layout} k={a.k}"), flush=True)
         return
     import torch.distributed as dist
@@ -97,7 +97,7 @@ def main():
     e.record()
     torch.cuda.synchronize()
     tr = comm.trace()
-    summ = summarize_ll if comm.protocol(n, a.dtype) == "ll" else summarize
+    summ = summarize_ll if comm.protocol(n, a.dtype) in ("ll", "ll128") else summarize
     txt = summ(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e) / a.calls:.4f} ms/call over {a.calls} calls")
     for r in range(dist.get_world_size()):
         if r == rank:
