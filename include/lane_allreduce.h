@@ -243,6 +243,13 @@ int lane_allreduce_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype,
  * (null), UNSUPPORTED (dtype). Host only. */
 int lane_allreduce_protocol(lane_comm_t comm, size_t count, lane_dtype_t dtype, int* protocol);
 
+/* *protocol receives the protocol lane_allreduce_ring (and _ring_emulated)
+ * uses for (count, dtype): LANE_PROTO_LL128 above $LANE_LL128_MIN_BYTES per
+ * rank (or with $LANE_PROTO=ll128), else LANE_PROTO_LL ($LANE_PROTO=ll forces
+ * it). Both give the same bits (same rounds, ring chunks and hop order).
+ * Errors: INVALID_ARG (null; plan does not fit), UNSUPPORTED (dtype). Host only. */
+int lane_allreduce_ring_protocol(lane_comm_t comm, size_t count, lane_dtype_t dtype, int* protocol);
+
 /* -------------------------------------------------- host-only introspection
  * No GPU needed; used by the CPU test-suite to compare the library's own
  * topology and partition with the oracle's. */

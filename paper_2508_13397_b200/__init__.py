@@ -92,6 +92,13 @@ class _CommBase:
         return {"chunk_granules": cg.value, "round_granules": rg.value, "ctas_per_group": C.value,
                 "launches": launches.value}
 
+    def ring_protocol(self, count: int, dtype: str = "float32") -> str:
+        """'ll' or 'll128': the protocol a ring allreduce (Alg. 1) call of this size uses."""
+        pr = ctypes.c_int()
+        _lib.check(_lib.load().lane_allreduce_ring_protocol(self._comm, count, DTYPE[dtype], ctypes.byref(pr)),
+                   self._comm)
+        return {1: "ll", 2: "ll128"}.get(pr.value, "simple")
+
     def protocol(self, count: int, dtype: str = "float32") -> str:
         """'ll', 'll128' or 'simple': the signalling protocol a call of this size uses."""
         pr = ctypes.c_int()

@@ -69,6 +69,7 @@ def load() -> ctypes.CDLL:
         "lane_allreduce_plan": (I, [P, SZ, I, ctypes.POINTER(I64), ctypes.POINTER(I64),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_allreduce_protocol": (I, [P, SZ, I, ctypes.POINTER(I)]),
+        "lane_allreduce_ring_protocol": (I, [P, SZ, I, ctypes.POINTER(I)]),
         "lane_topology_query": (I, [I, I, I, ctypes.POINTER(I), ctypes.POINTER(I),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_partition_query": (I, [U64, I, I, I, I, I64, I64, ctypes.POINTER(I64), U64,

@@ -332,6 +332,12 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     lo = lo < m0 ? lo : m0;
     lo = lo < m1 ? lo : m1;
     lo = lo < m2 ? lo : m2;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m0, lane::ll128::lane_ring_ll128_kernel<0>, lane::ll128::kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m1, lane::ll128::lane_ring_ll128_kernel<1>, lane::ll128::kThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m2, lane::ll128::lane_ring_ll128_kernel<2>, lane::ll128::kThreads, 0);
+    lo = lo < m0 ? lo : m0;
+    lo = lo < m1 ? lo : m1;
+    lo = lo < m2 ? lo : m2;
     c->ll_coresident = (lo < 1 ? 1 : lo) * c->sm_count;
   }
 
@@ -396,11 +402,12 @@ struct Plan {
   int rounds, C, tail_elems, q;
   int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
           // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan);
-          // 4: LL128 lane kernel, one launch; 5: "approach 2" (rounds, a2_plan)
+          // 4: LL128 lane kernel, one launch; 5: "approach 2" (rounds, a2_plan);
+          // 6: flat ring on the LL128 protocol (ring_plan)
 };
 
 // Plans whose rounds are LL-capacity sized (ll_ring_rounds launches them).
-bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5; }
+bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5 || pl.ll == 6; }
 
 bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
 bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl);
@@ -542,16 +549,23 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
   const int64_t nch = lane::n_chunks(lane::ceil_div(r0, c->k), cg);
   if (nch < C) C = (int)(nch > 0 ? nch : 1);
   const int64_t cap = lane::round_chunks(r0, c->k, cg);  // the first round is the largest
+  pl->C = C;
+  pl->cg = cg;
+  pl->rounds = (int)lane::ceil_div(ng, RC);
+  pl->round_len0 = r0;
+  // flat ring on LL128 lines (same rounds and chunks, hence the same bits):
+  // LANE_PROTO=ll128, or auto above LANE_LL128_MIN_BYTES
+  if (!lane_ring && c->ll128_set > 0 && c->proto != 1 && (c->proto == 3 || ng > c->ll128_lo) &&
+      lane::ll128::ring_set_lines(c->P, cap, lane::ll128::lines_of(lane::ceil_div(cg, c->P))) <= c->ll128_set) {
+    pl->ll = 6;
+    return true;
+  }
   if (lane_ring) {
     const int64_t sg = lane::ceil_div(cg, c->G), su = lane::ceil_div(sg, c->N);
     if (cap * sg > c->ll_slot_g || cap * su > c->ll_slot_u) return false;
   } else if (cap * lane::ceil_div(cg, c->P) > c->ring_slot) {
     return false;
   }
-  pl->C = C;
-  pl->cg = cg;
-  pl->rounds = (int)lane::ceil_div(ng, RC);
-  pl->round_len0 = r0;
   pl->ll = lane_ring ? 2 : 3;
   return true;
 }
@@ -589,17 +603,17 @@ bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
 // a2_plan (ll == 5).
 int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
   const int ranks_here = c->emulated ? c->P : 1;
-  const bool flat = pl.ll == 3, a2 = pl.ll == 5;
+  const bool flat = pl.ll == 3, a2 = pl.ll == 5, ring128 = pl.ll == 6;
   const int64_t RC = c->ll_max;
   p.ll_slot_g = flat ? c->ring_slot : c->ll_slot_g;
   p.ll_slot_u = flat ? 0 : (a2 ? c->a2_slot_v : c->ll_slot_u);
-  p.ll_set = c->ll_set;
+  p.ll_set = ring128 ? c->ll128_set : c->ll_set;
   p.ring2 = pl.ll == 2 ? 1 : 0;
   p.handshake = 0;
   p.direct = 0;
   p.C = pl.C;
   p.cg = pl.cg;
-  p.sg = lane::ceil_div(pl.cg, flat ? c->P : c->G);
+  p.sg = lane::ceil_div(pl.cg, (flat || ring128) ? c->P : c->G);
   p.su = flat ? 0 : (a2 ? lane::ceil_div(pl.cg, c->N) : lane::ceil_div(p.sg, c->N));
   c->trace_ctas = 0;
   for (int r = 0; r < pl.rounds; ++r) {
@@ -607,10 +621,15 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     const int64_t rest = pl.ng - p.round_g0;
     p.round_len = rest < RC ? rest : RC;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
+    if (ring128) p.ll_slot_g = p.cap * lane::ll128::lines_of(p.sg);  // lines per RS / AG slot
     p.epoch = ++c->epoch;
     void* args[] = {&p};
     const void* fn;
-    if (a2)
+    if (ring128)
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ring_ll128_kernel<0>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ring_ll128_kernel<1>
+                                   : (const void*)lane::ll128::lane_ring_ll128_kernel<2>;
+    else if (a2)
       fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_a2_ll_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_a2_ll_kernel<1>
                                    : (const void*)lane::ll::lane_a2_ll_kernel<2>;
@@ -626,7 +645,9 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
                                 : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
     if (e != cudaSuccess)
-      return cuda_fail(c, e, a2 ? "lane_a2_ll_kernel launch" : (flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch"));
+      return cuda_fail(c, e, ring128 ? "lane_ring_ll128_kernel launch"
+                             : a2    ? "lane_a2_ll_kernel launch"
+                                     : (flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch"));
   }
   return LANE_OK;
 }
@@ -1336,6 +1357,20 @@ int lane_allreduce_ring_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, in
   if (round_granules) *round_granules = c->ll_max;
   if (ctas_per_group) *ctas_per_group = pl.C;
   if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
+  return LANE_OK;
+}
+
+int lane_allreduce_ring_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int* protocol) {
+  if (!c || !protocol) return fail(c, LANE_ERR_INVALID_ARG, "ring_protocol: null argument");
+  if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
+    return fail(c, LANE_ERR_UNSUPPORTED, "dtype: unsupported lane_dtype_t");
+  const int q = 16 / itemsize_of(dtype);
+  Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  pl.ng = (int64_t)((count + q - 1) / q);
+  if (!ring_plan(c, pl.ng, false, &pl))
+    return fail(c, LANE_ERR_INVALID_ARG, "ring: procs_per_gpu exceeds the co-resident CTA capacity or inboxes");
+  *protocol = pl.ll == 6 ? LANE_PROTO_LL128 : LANE_PROTO_LL;
   return LANE_OK;
 }
 

@@ -408,5 +408,136 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
   ll::phase_clock_flush(p, pc);
 }
 
+
+// ========================================================================
+// Ring allreduce (Alg. 1 "ring_allreduce", P L150-206) on the LL128
+// protocol: same algorithm, chunking (fixed ring chunks, R#21), rounds (the
+// LL capacity, so both protocols give the same bits) and per-hop rounding
+// (R#11) as lane_ring_ll_kernel; the packet is a 128-byte line. Chunk c of
+// slice l is split into P ring parts (remainder-first); an 8-lane group
+// carries one line of every part (granules 7 ln .. 7 ln + 6 of the part)
+// through all 2(P-1) steps. Reduce-scatter step s: rank r sends its running
+// partial of part r-s to r+1's RS slot s and reduces part r-1-s received from
+// r-1 with its own sendbuf part; allgather step s: send part r+1-s to r+1's
+// AG slot s, receive part r-s.
+//
+// Inbox (per parity set): RS slots s = 0..P-2 then AG slots, each
+// p.ll_slot_g = cap * lp lines (lp = ceil(ceil(cg/P)/7) lines per ring part).
+LANE_HD int64_t ring_set_lines(int P, int64_t cap, int64_t lp) { return 2 * (int64_t)(P - 1) * cap * lp; }
+
+template <int DT>
+__global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __grid_constant__ LaneParams p) {
+  using O = Ops<DT>;
+  const int per_rank = p.k * p.C;
+  const int r = p.rank0 + (int)(blockIdx.x / per_rank);
+  const int l = (int)(blockIdx.x % per_rank) / p.C;
+  const int j = (int)(blockIdx.x % p.C);
+  const int P = p.P;
+  const uint32_t ep = p.epoch;
+  const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 3, sl = threadIdx.x & 7;
+  const int64_t lp = lines_of(p.sg);  // p.sg = ceil(cg / P): longest ring part
+  const uint4 z = make_uint4(0, 0, 0, 0);
+
+  Msg msg;
+  msg.send = reinterpret_cast<const uint4*>(p.rk[r].send);
+  msg.recv = reinterpret_cast<uint4*>(p.rk[r].recv);
+  msg.partial_g = p.tail_elems < p.q ? p.ng - 1 : -1;
+  msg.partial_bytes = p.tail_elems * (16 / p.q);
+
+  const Span sls = rf_split(p.round_len, p.k, l);
+  const int64_t nc = n_chunks(sls.len, p.cg);
+  const int64_t cb = chunk_base(p.round_len, p.k, l, p.cg);
+  const int64_t ncj = nc > j ? (nc - j + p.C - 1) / p.C : 0;  // chunks j, j+C, ... of this CTA
+  uint4* const mine = reinterpret_cast<uint4*>(p.rk[r].ll) + (int64_t)(ep & 1u) * p.ll_set * 8;
+  uint4* const next = reinterpret_cast<uint4*>(p.rk[(r + 1) % P].ll) + (int64_t)(ep & 1u) * p.ll_set * 8;
+  auto rs = [&](uint4* b, int s, int64_t id, int64_t ln) { return b + ((int64_t)s * p.ll_slot_g + id * lp + ln) * 8; };
+  auto ag = [&](uint4* b, int s, int64_t id, int64_t ln) {
+    return b + ((int64_t)(P - 1 + s) * p.ll_slot_g + id * lp + ln) * 8;
+  };
+  auto md = [&](int x) { return ((x % P) + P) % P; };
+
+  // flat space: (chunk of this CTA, line of a ring part); U lines per group per warp step
+  const int64_t total = ncj * lp;
+  for (int64_t V0 = (int64_t)warp * 4 * U; V0 < total; V0 += kWarps * 4 * U) {
+    bool on[U];
+    int64_t id[U], g0[U], ln[U], pb[U], pr[U];  // chunk, first granule, line, part base / remainder
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = V0 + 4 * u + grp;
+      on[u] = v < total;
+      const int64_t cc = on[u] ? v / lp : 0;
+      ln[u] = on[u] ? v - cc * lp : 0;
+      const int64_t c = j + cc * p.C;
+      id[u] = cb + c;
+      g0[u] = p.round_g0 + sls.start + c * p.cg;
+      const int64_t rest = sls.len - c * p.cg;
+      const int64_t clen = rest < p.cg ? rest : p.cg;
+      pb[u] = clen / P;
+      pr[u] = clen % P;
+    }
+    // part x of the chunk: start x*pb + min(x, pr), length pb + (x < pr)
+    auto pstart = [&](int u, int x) { return (int64_t)x * pb[u] + (x < pr[u] ? x : pr[u]); };
+    auto plen = [&](int u, int x) { return pb[u] + (x < pr[u] ? 1 : 0); };
+    auto act = [&](int u, int x) { return on[u] && ln[u] < lines_of(plen(u, x)); };
+    auto dv = [&](int u, int x) { return act(u, x) && sl < kLineGranules && ln[u] * kLineGranules + sl < plen(u, x); };
+    auto gidx = [&](int u, int x) { return g0[u] + pstart(u, x) + ln[u] * kLineGranules + sl; };
+
+    uint4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) v[u] = dv(u, r) ? load_x(msg, gidx(u, r)) : z;
+    // reduce-scatter loop (P L175-188)
+    for (int s = 0; s < P - 1; ++s) {
+      const int sp = md(r - s), rp = md(r - 1 - s);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act(u, sp)) line_store(rs(next, s, id[u], ln[u]), sl, v[u], ep);
+      const uint4* ptr[U];
+      bool a[U];
+      uint4 w[U], x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ptr[u] = rs(mine, s, id[u], ln[u]);
+        a[u] = act(u, rp);
+        x[u] = dv(u, rp) ? load_x(msg, gidx(u, rp)) : z;
+      }
+      if (!get_lines(p, ptr, a, sl, w)) return;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (a[u]) {
+          typename O::Acc acc;
+          O::init(acc, w[u]);
+          O::add(acc, x[u]);
+          v[u] = O::narrow(acc);  // one rounding per hop (R#11)
+        }
+    }
+    // rank r completed part r+1 (the last rp)
+#pragma unroll
+    for (int u = 0; u < U; ++u)
+      if (dv(u, md(r + 1))) store_out(msg, gidx(u, md(r + 1)), v[u]);
+    // allgather loop (P L190-203)
+    for (int s = 0; s < P - 1; ++s) {
+      const int sp = md(r + 1 - s), rp = md(r - s);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (act(u, sp)) line_store(ag(next, s, id[u], ln[u]), sl, v[u], ep);
+      const uint4* ptr[U];
+      bool a[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        ptr[u] = ag(mine, s, id[u], ln[u]);
+        a[u] = act(u, rp);
+      }
+      uint4 w[U];
+      if (!get_lines(p, ptr, a, sl, w)) return;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (a[u]) {
+          v[u] = w[u];
+          if (dv(u, rp)) store_out(msg, gidx(u, rp), v[u]);
+        }
+    }
+  }
+}
+
 }  // namespace ll128
 }  // namespace lane

@@ -105,8 +105,8 @@ def main():
                               f"reg={registered}: "
                               f"{len(bad)} mismatches first {idx[bad[:5]]}", flush=True)
                         failures += 1
-            # ring allreduce (Alg. 1) vs the ring oracle, on the same comm
-            if proto == "ll":
+            # ring allreduce (Alg. 1) vs the ring oracle, on the same comm (LL packets / LL128 lines)
+            if proto in ("ll", "ll128"):
                 for dtype, n in (("float32", 4099), ("bfloat16", (1 << 20) + 3), ("int32", 7)):
                     tdt = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}[dtype]
                     inp = sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, "signed", 5 + n, rank)

@@ -306,11 +306,15 @@ def run_ring(N, G, k, dtype, xs, inplace=False):
 
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-def test_ring_parity(P, dtype):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ring_parity(P, dtype, proto, monkeypatch):
     """Ring allreduce (Alg. 1, lane_allreduce_ring_emulated) vs the ring oracle,
-    bit-exact: ring order per chunk, one rounding per hop."""
+    bit-exact: ring order per chunk, one rounding per hop — on the LL packets
+    and on the LL128 lines (lane_ring_ll128_kernel)."""
+    monkeypatch.setenv("LANE_PROTO", proto)
     for k in (1, 2, 3):
         for n in COUNTS:
+            assert emu(1, P, k).ring_protocol(n, dtype) == proto
             xs = si.generate_all(dtype, "signed", 7 + n, P, n)
             got = run_ring(1, P, k, dtype, xs, inplace=(n % 2 == 1))
             pl = emu(1, P, k).plan(n, dtype, algorithm="ring")
@@ -319,10 +323,12 @@ def test_ring_parity(P, dtype):
                 assert np.array_equal(bits(o), bits(ref)), f"ring P={P} k={k} n={n} rank {p}"
 
 
-def test_ring_multi_round_and_interleaved_with_lane(monkeypatch):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_ring_multi_round_and_interleaved_with_lane(proto, monkeypatch):
     """Ring messages above the LL capacity run in several launches; ring and
     lane calls share the LL parity sets and the epoch counter."""
     monkeypatch.setenv("LANE_LL_MAX_BYTES", str(256 << 10))
+    monkeypatch.setenv("LANE_PROTO", proto)
     N, G, k = 2, 2, 2
     for it, n in enumerate([(1 << 18) + 9, 1000, (1 << 16) + 1, 77]):
         dtype = ["float32", "int32", "bfloat16", "float32"][it]
