@@ -78,6 +78,16 @@ def itemsize(dtype):
     return 2 if dtype == "bfloat16" else 4
 
 
+def max_over_ranks(ms):
+    """Device time of a multi-rank step: the MAX over ranks (every rank gets
+    it; torch.distributed, gloo or nccl)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def busbw(bytes_, P, ms):
     return bytes_ * 2 * (P - 1) / P / (ms * 1e-3) / 1e9 if P > 1 else bytes_ / (ms * 1e-3) / 1e9
 
@@ -452,9 +462,7 @@ def run_multi(args):
     if clk:
         clk.__exit__()
     comm.check()
-    t = torch.tensor([ms], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms)
     ok = sample_check([out], N, G, dtype, n, seed, [rank])
     okt = torch.tensor([0 if ok else 1])
     dist.all_reduce(okt)
@@ -520,10 +528,9 @@ def e2e_multi(comm, inp, N, G, dtype, n, S, args, dist):
     stream = torch.cuda.current_stream()
     ms = device_time_ms(lambda: comm.allreduce_host(h_out, h_in), args.e2e_steps, 1, stream,
                         lambda: dist.barrier())
-    t = torch.tensor([ms], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = max_over_ranks(ms)
     P = N * G
-    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 3),
+    return {"value": round(busbw(S, P, ms), 2), "unit": "GB/s", "ms_per_step": round(ms, 3),
             "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
             "api": "lane_allreduce_host (C ABI, pinned host buffers)"}
 
@@ -557,10 +564,9 @@ class NcclPPG:
 def nccl_ppg(inp, S, P, args, dist, stream, ppg_obj):
     import torch
     buf = inp.clone()
-    ms = device_time_ms(lambda: ppg_obj.run(buf, dist), args.steps, args.warmup, stream, lambda: dist.barrier())
-    t = torch.tensor([ms], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 4),
+    ms = max_over_ranks(device_time_ms(lambda: ppg_obj.run(buf, dist), args.steps, args.warmup, stream,
+                                       lambda: dist.barrier()))
+    return {"value": round(busbw(S, P, ms), 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "ppg": ppg_obj.ppg, "algo": os.environ.get("NCCL_ALGO", "default")}
 
 
@@ -568,10 +574,8 @@ def nccl_ring(inp, S, P, args, dist, stream):
     import torch
     buf = inp.clone()
     step = lambda: dist.all_reduce(buf)  # noqa: E731
-    ms = device_time_ms(step, args.steps, args.warmup, stream, lambda: dist.barrier())
-    t = torch.tensor([ms], dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return {"value": round(busbw(S, P, t.item()), 2), "unit": "GB/s", "ms_per_step": round(t.item(), 4),
+    ms = max_over_ranks(device_time_ms(step, args.steps, args.warmup, stream, lambda: dist.barrier()))
+    return {"value": round(busbw(S, P, ms), 2), "unit": "GB/s", "ms_per_step": round(ms, 4),
             "algo": os.environ.get("NCCL_ALGO", "default"), "version": ".".join(map(str, torch.cuda.nccl.version()))}
 
 
