@@ -332,6 +332,13 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     lo = lo < m0 ? lo : m0;
     lo = lo < m1 ? lo : m1;
     lo = lo < m2 ? lo : m2;
+    for (const void* f : {(const void*)lane::ll128::lane_ll128_kernel<0, true>,
+                          (const void*)lane::ll128::lane_ll128_kernel<1, true>,
+                          (const void*)lane::ll128::lane_ll128_kernel<2, true>}) {
+      int mr = 0;
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mr, f, lane::ll128::kThreads, 0);
+      lo = lo < mr ? lo : mr;
+    }
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m0, lane::ll128::lane_ring_ll128_kernel<0>, lane::ll128::kThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m1, lane::ll128::lane_ring_ll128_kernel<1>, lane::ll128::kThreads, 0);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&m2, lane::ll128::lane_ring_ll128_kernel<2>, lane::ll128::kThreads, 0);
@@ -403,11 +410,12 @@ struct Plan {
   int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
           // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan);
           // 4: LL128 lane kernel, one launch; 5: "approach 2" (rounds, a2_plan);
-          // 6: flat ring on the LL128 protocol (ring_plan)
+          // 6: flat ring on the LL128 protocol (ring_plan); 7: LL128 lane kernel
+          // with the ring inter-node stage (rounds, ring_plan)
 };
 
 // Plans whose rounds are LL-capacity sized (ll_ring_rounds launches them).
-bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5 || pl.ll == 6; }
+bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5 || pl.ll == 6 || pl.ll == 7; }
 
 bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
 bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl);
@@ -553,12 +561,17 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
   pl->cg = cg;
   pl->rounds = (int)lane::ceil_div(ng, RC);
   pl->round_len0 = r0;
-  // flat ring on LL128 lines (same rounds and chunks, hence the same bits):
-  // LANE_PROTO=ll128, or auto above LANE_LL128_MIN_BYTES
-  if (!lane_ring && c->ll128_set > 0 && c->proto != 1 && (c->proto == 3 || ng > c->ll128_lo) &&
-      lane::ll128::ring_set_lines(c->P, cap, lane::ll128::lines_of(lane::ceil_div(cg, c->P))) <= c->ll128_set) {
-    pl->ll = 6;
-    return true;
+  // ring algorithms on LL128 lines (same rounds and chunks, hence the same
+  // bits): LANE_PROTO=ll128, or auto above LANE_LL128_MIN_BYTES
+  if (c->ll128_set > 0 && c->proto != 1 && (c->proto == 3 || ng > c->ll128_lo)) {
+    const int64_t need =
+        lane_ring ? lane::ll128::set_lines(c->G, c->N, cap,
+                                           lane::ll128::lines_of(lane::ceil_div(lane::ceil_div(cg, c->G), c->N)))
+                  : lane::ll128::ring_set_lines(c->P, cap, lane::ll128::lines_of(lane::ceil_div(cg, c->P)));
+    if (need <= c->ll128_set) {
+      pl->ll = lane_ring ? 7 : 6;
+      return true;
+    }
   }
   if (lane_ring) {
     const int64_t sg = lane::ceil_div(cg, c->G), su = lane::ceil_div(sg, c->N);
@@ -603,12 +616,12 @@ bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
 // a2_plan (ll == 5).
 int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
   const int ranks_here = c->emulated ? c->P : 1;
-  const bool flat = pl.ll == 3, a2 = pl.ll == 5, ring128 = pl.ll == 6;
+  const bool flat = pl.ll == 3, a2 = pl.ll == 5, ring128 = pl.ll == 6, lane128 = pl.ll == 7;
   const int64_t RC = c->ll_max;
   p.ll_slot_g = flat ? c->ring_slot : c->ll_slot_g;
   p.ll_slot_u = flat ? 0 : (a2 ? c->a2_slot_v : c->ll_slot_u);
-  p.ll_set = ring128 ? c->ll128_set : c->ll_set;
-  p.ring2 = pl.ll == 2 ? 1 : 0;
+  p.ll_set = (ring128 || lane128) ? c->ll128_set : c->ll_set;
+  p.ring2 = (pl.ll == 2 || lane128) ? 1 : 0;
   p.handshake = 0;
   p.direct = 0;
   p.C = pl.C;
@@ -622,10 +635,18 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     p.round_len = rest < RC ? rest : RC;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
     if (ring128) p.ll_slot_g = p.cap * lane::ll128::lines_of(p.sg);  // lines per RS / AG slot
+    if (lane128) {  // lines per L1/L4 and per L2/L3 slot (lane_ll128.cuh Inbox128)
+      p.ll_slot_g = p.cap * c->N * lane::ll128::lines_of(p.su);
+      p.ll_slot_u = p.cap * lane::ll128::lines_of(p.su);
+    }
     p.epoch = ++c->epoch;
     void* args[] = {&p};
     const void* fn;
-    if (ring128)
+    if (lane128)
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0, true>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1, true>
+                                   : (const void*)lane::ll128::lane_ll128_kernel<2, true>;
+    else if (ring128)
       fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ring_ll128_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ring_ll128_kernel<1>
                                    : (const void*)lane::ll128::lane_ring_ll128_kernel<2>;
@@ -645,7 +666,8 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
                                 : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
     if (e != cudaSuccess)
-      return cuda_fail(c, e, ring128 ? "lane_ring_ll128_kernel launch"
+      return cuda_fail(c, e, lane128   ? "lane_ll128_kernel launch (ring inter-node stage)"
+                             : ring128 ? "lane_ring_ll128_kernel launch"
                              : a2    ? "lane_a2_ll_kernel launch"
                                      : (flat ? "lane_ring_ll_kernel launch" : "lane_ll_kernel launch"));
   }
@@ -1381,7 +1403,7 @@ int lane_allreduce_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int
   Plan pl;
   int st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
-  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : (pl.ll == 4 ? LANE_PROTO_LL128 : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE));
+  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : ((pl.ll == 4 || pl.ll == 7) ? LANE_PROTO_LL128 : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE));
   return LANE_OK;
 }
 

@@ -168,7 +168,9 @@ __device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem&
   return b;
 }
 
-template <int DT>
+// RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a separate
+// instantiation so the default kernel keeps its register budget.
+template <int DT, bool RING2 = false>
 __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_constant__ LaneParams p) {
   __shared__ uint64_t clk[8];
   const ll::PhaseClock pc = ll::phase_clock_begin(p, clk);
@@ -258,6 +260,118 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
     });
   }
   pc.end(1);
+
+  if constexpr (RING2) {
+    // ---------------- B'/C'/D' (LANE_PHASE2=ring): the inter-node stage is
+    // Alg. 1 among the lane members (P L401, L457; R#22), as in lane_ll.cuh:
+    // ring chunk t = sub-part t of part g, lane member a sends to a+1, RS
+    // step s uses slot L2[s], AG step s L3[s]; the node sum T1 (ascending h,
+    // one rounding) is formed on demand from the L1 lines; every completed
+    // line goes to recvbuf and to the node peers' L4 (phase 3). An 8-lane
+    // group carries line ln of every sub-part through all 2(N-1) steps.
+    const Inbox128 nxt = inbox_of(p, p.rk[((a + 1) % N) * G + g]);
+    for (int64_t c = j; c < nc; c += p.C) {
+      const ChunkGeo ch = geo(c);
+      const Span gp = rf_split(ch.len, G, g);
+      auto widest = [&](int, int) { return Span{0, rf_split(gp.len, N, 0).len}; };  // remainder-first: sub-part 0
+      const bool ok = walk(1, 1, widest, [&](const Batch& q) {
+        auto up = [&](int x) { return rf_split(gp.len, N, x); };
+        auto act = [&](int u, int x) { return q.act[u] && q.ln[u] < lines_of(up(x).len); };
+        auto dv = [&](int u, int x) {
+          return act(u, x) && sl < kLineGranules && q.ln[u] * kLineGranules + sl < up(x).len;
+        };
+        auto gidx = [&](int u, int x) { return ch.g0 + gp.start + up(x).start + q.ln[u] * kLineGranules + sl; };
+        // node sum of ring chunk x at this group's lines (warp-collective)
+        auto t1 = [&](int x, uint4 (&out)[U]) -> bool {
+          typename O::Acc acc[U];
+          bool a_[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) a_[u] = act(u, x);
+          for (int h = 0; h < G; ++h) {  // warp-uniform, ascending (R#7)
+            uint4 v[U];
+            if (h == g) {
+#pragma unroll
+              for (int u = 0; u < U; ++u) v[u] = dv(u, x) ? load_x(msg, gidx(u, x)) : z;
+            } else {
+              const uint4* ptr[U];
+#pragma unroll
+              for (int u = 0; u < U; ++u) ptr[u] = me.l1(slot_of(h, g), ch.id, x, q.ln[u]);
+              if (!get_lines(p, ptr, a_, sl, v)) return false;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (h == 0)
+                O::init(acc[u], v[u]);
+              else
+                O::add(acc[u], v[u]);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) out[u] = O::narrow(acc[u]);
+          return true;
+        };
+        auto deliver = [&](int x, const uint4 (&v)[U]) {  // final lines of ring chunk x: recvbuf + phase 3
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (dv(u, x)) store_out(msg, gidx(u, x), v[u]);
+            if (act(u, x))
+              for (int t2 = 1; t2 < G; ++t2) {
+                const int h = (g + t2) % G;
+                line_store(inbox_of(p, p.rk[a * G + h]).l4(slot_of(g, h), ch.id, x, q.ln[u]), sl, v[u], ep);
+              }
+          }
+        };
+        uint4 v[U];
+        if (!t1(a, v)) return false;
+        for (int s = 0; s < N - 1; ++s) {  // reduce-scatter loop (P L175-188)
+          const int sp = ((a - s) % N + N) % N, rp = ((a - 1 - s) % N + N) % N;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (act(u, sp)) line_store(nxt.l2(s, ch.id, q.ln[u]), sl, v[u], ep);
+          const uint4* ptr[U];
+          bool a_[U];
+          uint4 w[U], own[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            ptr[u] = me.l2(s, ch.id, q.ln[u]);
+            a_[u] = act(u, rp);
+          }
+          if (!get_lines(p, ptr, a_, sl, w)) return false;
+          if (!t1(rp, own)) return false;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (a_[u]) {
+              typename O::Acc acc;
+              O::init(acc, w[u]);
+              O::add(acc, own[u]);
+              v[u] = O::narrow(acc);  // one rounding per hop (R#11)
+            }
+        }
+        deliver((a + 1) % N, v);
+        for (int s = 0; s < N - 1; ++s) {  // allgather loop (P L190-203)
+          const int sp = ((a + 1 - s) % N + N) % N, rp = ((a - s) % N + N) % N;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (act(u, sp)) line_store(nxt.l3(s, ch.id, q.ln[u]), sl, v[u], ep);
+          const uint4* ptr[U];
+          bool a_[U];
+          uint4 w[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            ptr[u] = me.l3(s, ch.id, q.ln[u]);
+            a_[u] = act(u, rp);
+          }
+          if (!get_lines(p, ptr, a_, sl, w)) return false;
+#pragma unroll
+          for (int u = 0; u < U; ++u)
+            if (a_[u]) v[u] = w[u];
+          deliver(rp, v);
+        }
+        return true;
+      });
+      if (!ok) return;
+    }
+  } else {
 
   // ---------------- B: phase-1 reduce (ascending h) -> phase-2 reduce-scatter push
   // (t = 0..N-1 -> sub-part b = a+1+t: remote sub-parts first, own last)
@@ -381,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
       if (!ok) return;
     }
   pc.end(4);
+  }  // !RING2
 
   // ---------------- E: phase-3 allgather receive (t = 0..G-2 -> node peer h = g+1+t)
   for (int64_t c = j; c < nc; c += p.C) {

@@ -49,12 +49,13 @@ def main():
     t0 = time.time()
     maxb = max(counts) * 4
     for N, G, k, proto in [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
-                           for pr in ("simple", "pull", "ll", "ll128", "ring2")]:
+                           for pr in ("simple", "pull", "ll", "ll128", "ring2", "ring2_128")]:
         if True:
             # ll / ll128: every call that fits that protocol's inboxes
-            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "ll128": "ll128"}.get(proto, "ll")
+            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "ll128": "ll128",
+                                        "ring2_128": "ll128"}.get(proto, "ll")
             os.environ["LANE_DIRECT"] = "3" if proto == "pull" else "2"  # registered job set: push / pull-all
-            if proto == "ring2":  # the lane method with Alg. 1 as its inter-node stage
+            if proto.startswith("ring2"):  # the lane method with Alg. 1 as its inter-node stage
                 os.environ["LANE_PHASE2"] = "ring"
             else:
                 os.environ.pop("LANE_PHASE2", None)
@@ -87,7 +88,7 @@ def main():
                     else:
                         idx = si.sample_indices(n, 4099, [n // 2, n // 3])
                     xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(P)]
-                    if proto == "ring2":
+                    if proto.startswith("ring2"):
                         if n > (1 << 20) + 3:  # sampled indices: the ring order needs whole chunks; exact int only
                             if dtype != "int32":
                                 continue
@@ -136,7 +137,7 @@ def main():
                         failures += 1
             # host-buffer API (pipelined pieces, ragged tail; each piece is its own
             # allreduce, so only the direct stage's order is piece-independent)
-            if proto == "ring2":
+            if proto.startswith("ring2"):
                 dist.barrier()
                 comm.close()
                 dist.barrier()

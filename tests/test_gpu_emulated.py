@@ -344,15 +344,19 @@ def test_ring_multi_round_and_interleaved_with_lane(proto, monkeypatch):
 
 @pytest.mark.parametrize("N,G", [(2, 2), (4, 2), (8, 1), (1, 8), (2, 4), (3, 2), (4, 1)])
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-def test_lane_ring_phase2_parity(N, G, dtype, monkeypatch):
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+def test_lane_ring_phase2_parity(N, G, dtype, proto, monkeypatch):
     """LANE_PHASE2=ring: the lane method with Alg. 1 as the inter-node stage
     (fig:full_mpi_comparison) vs the oracle's ring variant, bit-exact, with
-    small ring chunks and LL rounds so several chunks and launches occur."""
+    small ring chunks and LL rounds so several chunks and launches occur —
+    on the LL packets and on LL128 lines."""
     monkeypatch.setenv("LANE_PHASE2", "ring")
+    monkeypatch.setenv("LANE_PROTO", proto)
     monkeypatch.setenv("LANE_RING_CHUNK_BYTES", str(8 << 10))
     monkeypatch.setenv("LANE_LL_MAX_BYTES", str(512 << 10))
     for k in (1, 3):
         for n in (1, 7, 4099, (1 << 17) + 5):
+            assert emu(N, G, k).protocol(n, dtype) == proto
             xs = si.generate_all(dtype, "signed", 3 + n, N * G, n)
             got = run(N, G, k, dtype, xs, inplace=(n == 7))
             pl = emu(N, G, k).plan(n, dtype)
