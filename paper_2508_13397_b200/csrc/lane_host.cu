@@ -562,8 +562,10 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
   pl->rounds = (int)lane::ceil_div(ng, RC);
   pl->round_len0 = r0;
   // ring algorithms on LL128 lines (same rounds and chunks, hence the same
-  // bits): LANE_PROTO=ll128, or auto above LANE_LL128_MIN_BYTES
-  if (c->ll128_set > 0 && c->proto != 1 && (c->proto == 3 || ng > c->ll128_lo)) {
+  // bits): LANE_PROTO=ll128; auto above LANE_LL128_MIN_BYTES for the flat
+  // ring only (the lane kernel's ring stage measured no faster on LL128:
+  // profiles/r01_sizes_lane_ring2_ll128.txt)
+  if (c->ll128_set > 0 && c->proto != 1 && (c->proto == 3 || (!lane_ring && ng > c->ll128_lo))) {
     const int64_t need =
         lane_ring ? lane::ll128::set_lines(c->G, c->N, cap,
                                            lane::ll128::lines_of(lane::ceil_div(lane::ceil_div(cg, c->G), c->N)))
