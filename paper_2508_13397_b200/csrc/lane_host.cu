@@ -92,6 +92,7 @@ struct lane_comm_s {
   int64_t ll128_hi = 0;      // ... up to this size
   int64_t ll128_cg_min = 0;  // granules
   int64_t ll128_set = 0;     // lines (128 B) per LL128 parity set
+  int64_t ll128_u1_max = 0;  // granules: LL128 lane kernel with U = 1 up to this size, U = 2 above
   uint64_t ll_bytes = 0;
   std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
   std::vector<void*> opened; // IPC-opened peer allocations
@@ -297,6 +298,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   c->ll128_lo = env_i64("LANE_LL128_MIN_BYTES", (N * G == 2 ? 2 : 1) << 20) / 16;
   c->ll128_hi = env_i64("LANE_LL128_THRESHOLD_BYTES", 16 << 20) / 16;
   c->ll128_cg_min = env_i64("LANE_LL128_MIN_CHUNK_BYTES", 16 << 10) / 16;
+  c->ll128_u1_max = env_i64("LANE_LL128_U1_MAX_BYTES", 4 << 20) / 16;
   if (c->ll128_cg_min < 64) c->ll128_cg_min = 64;
   c->ll_max = env_i64("LANE_LL_MAX_BYTES", 16 << 20) / 16;
   if (c->ll_max < 0) c->ll_max = 0;
@@ -332,7 +334,10 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     lo = lo < m0 ? lo : m0;
     lo = lo < m1 ? lo : m1;
     lo = lo < m2 ? lo : m2;
-    for (const void* f : {(const void*)lane::ll128::lane_ll128_kernel<0, true>,
+    for (const void* f : {(const void*)lane::ll128::lane_ll128_kernel<0, false, 1>,
+                          (const void*)lane::ll128::lane_ll128_kernel<1, false, 1>,
+                          (const void*)lane::ll128::lane_ll128_kernel<2, false, 1>,
+                          (const void*)lane::ll128::lane_ll128_kernel<0, true>,
                           (const void*)lane::ll128::lane_ll128_kernel<1, true>,
                           (const void*)lane::ll128::lane_ll128_kernel<2, true>}) {
       int mr = 0;
@@ -698,9 +703,13 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
       p.direct = 0;
       c->trace_ctas = (int)grid.x;
       void* args[] = {&p};
-      const void* fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0>
-                       : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1>
-                                               : (const void*)lane::ll128::lane_ll128_kernel<2>;
+      const bool u1 = pl.ng <= c->ll128_u1_max;  // small messages: one line per group per warp step
+      const void* fn = u1 ? (dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0, false, 1>
+                             : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1, false, 1>
+                                                     : (const void*)lane::ll128::lane_ll128_kernel<2, false, 1>)
+                          : (dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0>
+                             : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1>
+                                                     : (const void*)lane::ll128::lane_ll128_kernel<2>);
       cudaError_t e = c->emulated
                           ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s)
                           : cudaLaunchKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s);

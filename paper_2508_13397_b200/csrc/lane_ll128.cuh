@@ -99,15 +99,18 @@ __device__ __noinline__ bool wait_line(const LaneParams& p, const uint4* line, i
   }
 }
 
-#ifndef LANE_LL128_U  // lines per 8-lane group per warp step (loads in flight per lane)
+// U: lines per 8-lane group per warp step (loads in flight per lane); a
+// template parameter of the kernels: the host takes U = 1 for small messages
+// (one warp step covers fewer lines, so more warps get work) and U = 2 above.
+#ifndef LANE_LL128_U
 #define LANE_LL128_U 2
 #endif
-constexpr int U = LANE_LL128_U;
 
 // A warp step's U lines per 8-lane group: flat position, the line's
 // pointer(s), whether the line exists (act) and whether this lane holds a data
 // granule of its span (dv).
-struct Batch {
+template <int U>
+struct BatchT {
   bool act[U], dv[U];
   int t[U], b[U];
   int64_t ln[U], i[U];
@@ -115,6 +118,7 @@ struct Batch {
 
 // Warp-collective: fetch U lines (inactive lines read as zero, never loaded)
 // and wait until every active line carries the epoch.
+template <int U>
 __device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U], int sl,
                                           uint4 (&v)[U]) {
   bool got[U], all = true;
@@ -170,8 +174,9 @@ __device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem&
 
 // RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a separate
 // instantiation so the default kernel keeps its register budget.
-template <int DT, bool RING2 = false>
+template <int DT, bool RING2 = false, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_constant__ LaneParams p) {
+  using Batch = BatchT<U>;
   __shared__ uint64_t clk[8];
   const ll::PhaseClock pc = ll::phase_clock_begin(p, clk);
   using O = Ops<DT>;
@@ -540,7 +545,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
 // p.ll_slot_g = cap * lp lines (lp = ceil(ceil(cg/P)/7) lines per ring part).
 LANE_HD int64_t ring_set_lines(int P, int64_t cap, int64_t lp) { return 2 * (int64_t)(P - 1) * cap * lp; }
 
-template <int DT>
+template <int DT, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __grid_constant__ LaneParams p) {
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
