@@ -94,6 +94,7 @@ struct lane_comm_s {
   int64_t ll128_set = 0;     // lines (128 B) per LL128 parity set
   int64_t ll128_u1_max = 0;  // granules: LL128 lane kernel with U = 1 up to this size, U = 2 above
   uint64_t ll_bytes = 0;
+  uint64_t ll128_bytes = 0;  // LL128 region: its own (never shared with the LL packets, see carve)
   std::vector<char*> own;    // own scratch allocations (1, or P when emulated)
   std::vector<void*> opened; // IPC-opened peer allocations
   RankMem rk[LANE_MAX_RANKS];
@@ -210,12 +211,12 @@ void size_scratch(lane_comm_t c) {
     const int64_t chunks = M8 / c->ll128_cg_min + k + 1;
     c->ll128_set = 2 * lane::ceil_div(M8 + M8 / 4 + k * c->ll128_cg_min + chunks * G * N, lane::ll128::kLineGranules) +
                    2 * G * N * chunks + 64;
-    const uint64_t b8 = al((uint64_t)(2 * c->ll128_set) * lane::ll128::kLineBytes);
-    if (b8 > c->ll_bytes) c->ll_bytes = b8;
+    c->ll128_bytes = al((uint64_t)(2 * c->ll128_set) * lane::ll128::kLineBytes);
   } else {
     c->ll128_set = 0;
+    c->ll128_bytes = 0;
   }
-  c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes;
+  c->total_bytes = c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes + c->ll128_bytes;
 }
 
 void carve(lane_comm_t c, char* base, RankMem* m) {
@@ -224,6 +225,13 @@ void carve(lane_comm_t c, char* base, RankMem* m) {
   m->r = base + c->s1_bytes + c->s2_bytes;
   m->flags = reinterpret_cast<uint32_t*>(base + c->s1_bytes + c->s2_bytes + c->r_bytes);
   m->ll = c->ll_bytes ? base + c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes : nullptr;
+  // The LL128 lines get their own region: in it the last 16 bytes of every
+  // 128-byte line only ever hold epochs (every LL128 layout is line-aligned),
+  // and the LL region's packets only ever hold epochs in their high words. A
+  // shared region would let one protocol's user data sit where the other
+  // reads its epoch, so data equal to the current epoch could pass for a
+  // fresh packet.
+  m->ll128 = c->ll128_bytes ? base + c->s1_bytes + c->s2_bytes + c->r_bytes + c->flag_bytes + c->ll_bytes : nullptr;
   m->send = nullptr;
   m->recv = nullptr;
 }
@@ -359,7 +367,8 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     LANE_CUDA(c, cudaMalloc(&p, c->total_bytes));
     c->own.push_back(p);
     // flags must read 0 before any peer can write an epoch >= 1
-    LANE_CUDA(c, cudaMemset(p + c->s1_bytes + c->s2_bytes + c->r_bytes, 0, c->flag_bytes + c->ll_bytes));
+    LANE_CUDA(c, cudaMemset(p + c->s1_bytes + c->s2_bytes + c->r_bytes, 0,
+                            c->flag_bytes + c->ll_bytes + c->ll128_bytes));
   }
   LANE_CUDA(c, cudaHostAlloc(&c->err_host, 64, cudaHostAllocMapped));
   memset(c->err_host, 0, 64);

@@ -163,7 +163,7 @@ struct Inbox128 {
 // per slot for this call (host: cap * N * lu, cap * lu).
 __device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem& m) {
   Inbox128 b;
-  b.base = reinterpret_cast<uint4*>(m.ll) + (int64_t)(p.epoch & 1u) * p.ll_set * 8;
+  b.base = reinterpret_cast<uint4*>(m.ll128) + (int64_t)(p.epoch & 1u) * p.ll_set * 8;
   b.slot_g = p.ll_slot_g;
   b.slot_u = p.ll_slot_u;
   b.lu = lines_of(p.su);
@@ -568,8 +568,8 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
   const int64_t nc = n_chunks(sls.len, p.cg);
   const int64_t cb = chunk_base(p.round_len, p.k, l, p.cg);
   const int64_t ncj = nc > j ? (nc - j + p.C - 1) / p.C : 0;  // chunks j, j+C, ... of this CTA
-  uint4* const mine = reinterpret_cast<uint4*>(p.rk[r].ll) + (int64_t)(ep & 1u) * p.ll_set * 8;
-  uint4* const next = reinterpret_cast<uint4*>(p.rk[(r + 1) % P].ll) + (int64_t)(ep & 1u) * p.ll_set * 8;
+  uint4* const mine = reinterpret_cast<uint4*>(p.rk[r].ll128) + (int64_t)(ep & 1u) * p.ll_set * 8;
+  uint4* const next = reinterpret_cast<uint4*>(p.rk[(r + 1) % P].ll128) + (int64_t)(ep & 1u) * p.ll_set * 8;
   auto rs = [&](uint4* b, int s, int64_t id, int64_t ln) { return b + ((int64_t)s * p.ll_slot_g + id * lp + ln) * 8; };
   auto ag = [&](uint4* b, int s, int64_t id, int64_t ln) {
     return b + ((int64_t)(P - 1 + s) * p.ll_slot_g + id * lp + ln) * 8;

@@ -67,6 +67,7 @@ struct RankMem {
   char* r;           // lane result R: cap chunks x SG granules
   uint32_t* flags;   // F1[G][cap] F2[N][cap] F3[N][cap] F4[G][cap]
   char* ll;          // low-latency (LL) inboxes: 2 parity sets, see lane_ll.cuh
+  char* ll128;       // LL128 inboxes: 2 parity sets of 128-byte lines, see lane_ll128.cuh
   const char* send;  // user buffers (only for ranks this launch executes)
   char* recv;
 };
