@@ -227,8 +227,9 @@ int lane_allreduce_plan(lane_comm_t comm, size_t count, lane_dtype_t dtype,
  * (large messages; §3.1.2 phases as chunked jobs). LL: every 16-byte
  * granule travels as a 32-byte packet of four {data, epoch} 64-bit words, so
  * the reader's poll on the data is the signal (no fences; 2x NVLink bytes;
- * used up to $LANE_LL_THRESHOLD_BYTES, default 8 MiB per rank, and at most
- * $LANE_LL_MAX_BYTES, default 16 MiB, the LL inbox capacity). LL128: every
+ * used up to $LANE_LL_THRESHOLD_BYTES, default 8 MiB per rank, where LL128 does
+ * not take the call, and at most $LANE_LL_MAX_BYTES, default 16 MiB, the LL
+ * inbox capacity). LL128: every
  * 128-byte line carries 7 granules and the epoch (lane_ll128.cuh: 8 lanes of a
  * warp write and read the line in one 16-byte-per-lane instruction; 8/7 of the
  * bytes; used above $LANE_LL128_MIN_BYTES up to $LANE_LL128_THRESHOLD_BYTES
