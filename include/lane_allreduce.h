@@ -269,6 +269,24 @@ int lane_partition_query(uint64_t count, int itemsize, int nodes, int gpus_per_n
                          int procs_per_gpu, int64_t chunk_granules, int64_t round_granules,
                          int64_t* units_out, uint64_t max_units, uint64_t* n_units);
 
+/* LL128 planner of a one-round message of `granules` 16-byte granules
+ * (lane_ll128.cuh plan128), for procs_per_gpu CTA groups of at most
+ * ctas_per_group CTAs and the $LANE_LL128_MAX_BYTES / _MIN_CHUNK_BYTES
+ * settings: out[0..5] = {CTAs per group, chunk granules, chunks, lines per
+ * sub-part, lines per parity set the call needs, lines per set allocated}.
+ * The call runs on LL128 only if out[4] <= out[5]. Errors: INVALID_ARG. */
+int lane_ll128_plan_query(int nodes, int gpus_per_node, int procs_per_gpu, int64_t granules, int ctas_per_group,
+                          int64_t max_bytes, int64_t min_chunk_bytes, int64_t* out);
+
+/* Index, within an LL128 parity set, of the 128-byte line `line` of lane
+ * sub-part b of chunk `chunk` in inbox `kind` (1 = L1 phase-1 part from node
+ * peer slot, 2 = L2 lane RS slot, 3 = L3 lane AG slot, 4 = L4 phase-3 part
+ * from node peer slot; b ignored for 2 / 3) for a call with `chunks` chunks
+ * and lines_per_subpart lines per sub-part (lane_ll128.cuh layout128).
+ * Errors: INVALID_ARG (any index out of its range). */
+int lane_ll128_line_query(int nodes, int gpus_per_node, int64_t chunks, int64_t lines_per_subpart, int kind, int slot,
+                          int64_t chunk, int b, int64_t line, int64_t* index);
+
 /* Library version string. */
 const char* lane_allreduce_version(void);
 

@@ -70,6 +70,8 @@ def load() -> ctypes.CDLL:
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_allreduce_protocol": (I, [P, SZ, I, ctypes.POINTER(I)]),
         "lane_allreduce_ring_protocol": (I, [P, SZ, I, ctypes.POINTER(I)]),
+        "lane_ll128_plan_query": (I, [I, I, I, I64, I, I64, I64, ctypes.POINTER(I64)]),
+        "lane_ll128_line_query": (I, [I, I, I64, I64, I, I, I64, I, I64, ctypes.POINTER(I64)]),
         "lane_topology_query": (I, [I, I, I, ctypes.POINTER(I), ctypes.POINTER(I),
                                     ctypes.POINTER(I), ctypes.POINTER(I)]),
         "lane_partition_query": (I, [U64, I, I, I, I, I64, I64, ctypes.POINTER(I64), U64,

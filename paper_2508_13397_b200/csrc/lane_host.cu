@@ -208,9 +208,7 @@ void size_scratch(lane_comm_t c) {
   // falls back to another protocol.
   const int64_t M8 = c->ll128_max;
   if (M8 > 0) {
-    const int64_t chunks = M8 / c->ll128_cg_min + k + 1;
-    c->ll128_set = 2 * lane::ceil_div(M8 + M8 / 4 + k * c->ll128_cg_min + chunks * G * N, lane::ll128::kLineGranules) +
-                   2 * G * N * chunks + 64;
+    c->ll128_set = lane::ll128::set_capacity128((int)G, (int)N, (int)k, M8, c->ll128_cg_min);
     c->ll128_bytes = al((uint64_t)(2 * c->ll128_set) * lane::ll128::kLineBytes);
   } else {
     c->ll128_set = 0;
@@ -472,20 +470,10 @@ bool ll128_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   int C = budget / (ranks_here * c->k);
   if (C < 1) C = 1;
   if ((int64_t)C * c->k * ranks_here > c->ll_coresident) return false;  // every CTA must be resident
-  const int64_t slice0 = (ng + c->k - 1) / c->k;
-  int64_t cg = (slice0 + C - 1) / C;
-  // k*CG <= M/4 keeps the inbox sizing bound (size_scratch): with fewer than
-  // 4 CTAs per slice, CTAs take several chunks (phase-major)
-  const int64_t cg_cap = c->ll128_max / (4 * c->k);
-  if (cg > cg_cap) cg = cg_cap;
-  if (cg < c->ll128_cg_min) cg = c->ll128_cg_min;
-  const int64_t nch = lane::n_chunks(slice0, cg);
-  if (nch < C) C = (int)(nch > 0 ? nch : 1);
-  const int64_t cap = lane::round_chunks(ng, c->k, cg);
-  const int64_t lu = lane::ll128::lines_of(lane::ceil_div(lane::ceil_div(cg, c->G), c->N));
-  if (lane::ll128::set_lines(c->G, c->N, cap, lu) > c->ll128_set) return false;
-  pl->C = C;
-  pl->cg = cg;
+  const lane::ll128::Plan128 g = lane::ll128::plan128(c->G, c->N, c->k, ng, C, c->ll128_max, c->ll128_cg_min);
+  if (g.need > c->ll128_set) return false;
+  pl->C = g.C;
+  pl->cg = g.cg;
   pl->ll = 4;
   return true;
 }
@@ -650,11 +638,9 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     const int64_t rest = pl.ng - p.round_g0;
     p.round_len = rest < RC ? rest : RC;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
-    if (ring128) p.ll_slot_g = p.cap * lane::ll128::lines_of(p.sg);  // lines per RS / AG slot
-    if (lane128) {  // lines per L1/L4 and per L2/L3 slot (lane_ll128.cuh Inbox128)
-      p.ll_slot_g = p.cap * c->N * lane::ll128::lines_of(p.su);
-      p.ll_slot_u = p.cap * lane::ll128::lines_of(p.su);
-    }
+    // lines per RS / AG slot of the LL128 ring (the LL128 lane kernel derives
+    // its layout from p.cap and p.su: lane_ll128.cuh layout128)
+    if (ring128) p.ll_slot_g = p.cap * lane::ll128::lines_of(p.sg);
     p.epoch = ++c->epoch;
     void* args[] = {&p};
     const void* fn;
@@ -704,10 +690,7 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
     if (pl.ll == 4) {  // LL128 protocol: one launch, no scratch flags, no handshake
-      const int64_t lu = lane::ll128::lines_of(p.su);
-      p.ll_slot_g = p.cap * c->N * lu;
-      p.ll_slot_u = p.cap * lu;
-      p.ll_set = c->ll128_set;
+      p.ll_set = c->ll128_set;  // set stride; the layout follows from p.cap, p.su (layout128)
       p.handshake = 0;
       p.direct = 0;
       c->trace_ctas = (int)grid.x;
@@ -1400,6 +1383,47 @@ int lane_allreduce_ring_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, in
   if (ctas_per_group) *ctas_per_group = pl.C;
   if (launches) *launches = count == 0 ? 0 : (c->P == 1 ? 1 : pl.rounds);
   return LANE_OK;
+}
+
+int lane_ll128_plan_query(int nodes, int gpus_per_node, int procs_per_gpu, int64_t granules, int ctas_per_group,
+                          int64_t max_bytes, int64_t min_chunk_bytes, int64_t* out) {
+  std::string why;
+  int st = validate_topology(nodes, gpus_per_node, procs_per_gpu, &why);
+  if (st != LANE_OK) return st;
+  if (!out || granules < 0 || ctas_per_group < 1 || max_bytes < 16 || min_chunk_bytes < 16)
+    return LANE_ERR_INVALID_ARG;
+  const int64_t M = max_bytes / 16, cgm = min_chunk_bytes / 16;
+  const lane::ll128::Plan128 g =
+      lane::ll128::plan128(gpus_per_node, nodes, procs_per_gpu, granules, ctas_per_group, M, cgm);
+  out[0] = g.C;
+  out[1] = g.cg;
+  out[2] = g.cap;
+  out[3] = g.lu;
+  out[4] = g.need;
+  out[5] = lane::ll128::set_capacity128(gpus_per_node, nodes, procs_per_gpu, M, cgm);
+  return LANE_OK;
+}
+
+int lane_ll128_line_query(int nodes, int gpus_per_node, int64_t chunks, int64_t lines_per_subpart, int kind, int slot,
+                          int64_t chunk, int b, int64_t line, int64_t* index) {
+  const int N = nodes, G = gpus_per_node;
+  if (!index || N < 1 || G < 1 || chunks < 1 || lines_per_subpart < 1) return LANE_ERR_INVALID_ARG;
+  if (chunk < 0 || chunk >= chunks || line < 0 || line >= lines_per_subpart) return LANE_ERR_INVALID_ARG;
+  const lane::ll128::Layout128 y = lane::ll128::layout128(G, N, chunks, lines_per_subpart);
+  switch (kind) {
+    case 1:
+    case 4:
+      if (slot < 0 || slot >= G - 1 || b < 0 || b >= N) return LANE_ERR_INVALID_ARG;
+      *index = kind == 1 ? y.l1(slot, chunk, b, line) : y.l4(slot, chunk, b, line);
+      return LANE_OK;
+    case 2:
+    case 3:
+      if (slot < 0 || slot >= N) return LANE_ERR_INVALID_ARG;
+      *index = kind == 2 ? y.l2(slot, chunk, line) : y.l3(slot, chunk, line);
+      return LANE_OK;
+    default:
+      return LANE_ERR_INVALID_ARG;
+  }
 }
 
 int lane_allreduce_ring_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int* protocol) {

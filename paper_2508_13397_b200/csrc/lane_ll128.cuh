@@ -138,38 +138,93 @@ __device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* cons
   return true;
 }
 
-// Line addresses of one rank's inbox (current parity set).
-struct Inbox128 {
-  uint4* base;             // set base (16-byte units)
+// Line index within a parity set of the lane kernel's inboxes for a call
+// with cap chunks and lu lines per sub-part: (G-1) L1 slots, N L2 slots, N L3
+// slots, (G-1) L4 slots; an L1/L4 slot is cap chunks x N sub-parts x lu
+// lines, an L2/L3 slot cap chunks x lu lines. Host and device (the CPU tests
+// check through lane_ll128_line_query that it tiles [0, set_lines) exactly).
+struct Layout128 {
   int64_t slot_g, slot_u;  // lines per L1/L4 slot and per L2/L3 slot
   int64_t lu;              // lines per sub-part
   int G, N;
-  __device__ __forceinline__ uint4* at(int64_t line) const { return base + line * 8; }
-  __device__ __forceinline__ uint4* l1(int s, int64_t c, int b, int64_t ln) const {
-    return at((int64_t)s * slot_g + (c * N + b) * lu + ln);
+  LANE_HD int64_t l1(int s, int64_t c, int b, int64_t ln) const { return (int64_t)s * slot_g + (c * N + b) * lu + ln; }
+  LANE_HD int64_t l2(int b, int64_t c, int64_t ln) const {
+    return (int64_t)(G - 1) * slot_g + (int64_t)b * slot_u + c * lu + ln;
   }
-  __device__ __forceinline__ uint4* l2(int b, int64_t c, int64_t ln) const {
-    return at((int64_t)(G - 1) * slot_g + (int64_t)b * slot_u + c * lu + ln);
+  LANE_HD int64_t l3(int b, int64_t c, int64_t ln) const {
+    return (int64_t)(G - 1) * slot_g + (int64_t)(N + b) * slot_u + c * lu + ln;
   }
-  __device__ __forceinline__ uint4* l3(int b, int64_t c, int64_t ln) const {
-    return at((int64_t)(G - 1) * slot_g + (int64_t)(N + b) * slot_u + c * lu + ln);
-  }
-  __device__ __forceinline__ uint4* l4(int s, int64_t c, int b, int64_t ln) const {
-    return at((int64_t)(G - 1) * slot_g + (int64_t)(2 * N) * slot_u + (int64_t)s * slot_g + (c * N + b) * lu + ln);
+  LANE_HD int64_t l4(int s, int64_t c, int b, int64_t ln) const {
+    return (int64_t)(G - 1) * slot_g + (int64_t)(2 * N) * slot_u + (int64_t)s * slot_g + (c * N + b) * lu + ln;
   }
 };
 
-// p.ll_set = lines per parity set (stride), p.ll_slot_g / ll_slot_u = lines
-// per slot for this call (host: cap * N * lu, cap * lu).
+LANE_HD Layout128 layout128(int G, int N, int64_t cap, int64_t lu) {
+  Layout128 y;
+  y.slot_g = cap * N * lu;
+  y.slot_u = cap * lu;
+  y.lu = lu;
+  y.G = G;
+  y.N = N;
+  return y;
+}
+
+// Line addresses of one rank's inbox (current parity set).
+struct Inbox128 {
+  uint4* base;  // set base (16-byte units)
+  Layout128 y;
+  __device__ __forceinline__ uint4* at(int64_t line) const { return base + line * 8; }
+  __device__ __forceinline__ uint4* l1(int s, int64_t c, int b, int64_t ln) const { return at(y.l1(s, c, b, ln)); }
+  __device__ __forceinline__ uint4* l2(int b, int64_t c, int64_t ln) const { return at(y.l2(b, c, ln)); }
+  __device__ __forceinline__ uint4* l3(int b, int64_t c, int64_t ln) const { return at(y.l3(b, c, ln)); }
+  __device__ __forceinline__ uint4* l4(int s, int64_t c, int b, int64_t ln) const { return at(y.l4(s, c, b, ln)); }
+};
+
+// p.ll_set = lines per parity set (stride); p.cap chunks, lu from p.su.
 __device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem& m) {
   Inbox128 b;
   b.base = reinterpret_cast<uint4*>(m.ll128) + (int64_t)(p.epoch & 1u) * p.ll_set * 8;
-  b.slot_g = p.ll_slot_g;
-  b.slot_u = p.ll_slot_u;
-  b.lu = lines_of(p.su);
-  b.G = p.G;
-  b.N = p.N;
+  b.y = layout128(p.G, p.N, p.cap, lines_of(p.su));
   return b;
+}
+
+// ------------------------------------------------------------------ host planner
+// One-round LL128 call of ng granules, k CTA groups of at most C CTAs, inbox
+// capacity M granules of message, minimum chunk cg_min: CTAs per group,
+// chunk size (one chunk per CTA, k*CG <= M/4 — the sizing bound below), chunk
+// count, lines per sub-part, and lines per parity set the call uses.
+struct Plan128 {
+  int C;
+  int64_t cg, cap, lu, need;
+};
+
+inline Plan128 plan128(int G, int N, int k, int64_t ng, int C, int64_t M, int64_t cg_min) {
+  Plan128 o;
+  if (C < 1) C = 1;
+  const int64_t slice0 = (ng + k - 1) / k;
+  int64_t cg = (slice0 + C - 1) / C;
+  // k*CG <= M/4 keeps the inbox sizing bound (set_capacity128): with fewer
+  // than 4 CTAs per slice, CTAs take several chunks (phase-major)
+  const int64_t cg_cap = M / (4 * k);
+  if (cg > cg_cap) cg = cg_cap;
+  if (cg < cg_min) cg = cg_min;
+  const int64_t nch = n_chunks(slice0, cg);
+  if (nch < C) C = (int)(nch > 0 ? nch : 1);
+  o.C = C;
+  o.cg = cg;
+  o.cap = round_chunks(ng, k, cg);
+  o.lu = lines_of(ceil_div(ceil_div(cg, G), N));
+  o.need = set_lines(G, N, o.cap, o.lu);
+  return o;
+}
+
+// Lines per parity set allocated at init. A call needs 2*G*N*cap*lu lines;
+// with G*N*su <= CG + G*N and cap*CG <= M + k*CG this is at most
+// 2*(M + k*CG + cap*G*N)/7 + 2*cap*G*N lines; sized for k*CG <= M/4 (which
+// plan128 keeps unless CG is the minimum chunk, covered by the k*cg_min term).
+inline int64_t set_capacity128(int G, int N, int k, int64_t M, int64_t cg_min) {
+  const int64_t chunks = M / cg_min + k + 1;
+  return 2 * ceil_div(M + M / 4 + k * cg_min + chunks * G * N, kLineGranules) + 2 * (int64_t)G * N * chunks + 64;
 }
 
 // RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a separate

@@ -18,7 +18,7 @@ import paper_2508_13397_b200 as lane
 def test_library_exports_every_header_symbol():
     lib = _lib.load()
     syms = _lib.header_symbols()
-    assert len(syms) == 27, syms
+    assert len(syms) == 29, syms
     for s in syms:
         assert hasattr(lib, s), f"{s} declared in include/lane_allreduce.h but not exported"
     assert "sm_100a" in lane.version()
