@@ -26,7 +26,11 @@
 //   L2[b] b < N   : sub-part a of part g, node sum of (b,g), lu lines
 //   L3[b] b < N   : sub-part b of part g, lane result of (b,g), lu lines
 //   L4[s] s < G-1 : part h from node peer h, N sub-parts x lu lines
-// Phases (A..E) and the parity-set argument are those of lane_ll.cuh.
+// Phases (A..E) and the parity-set argument are those of lane_ll.cuh. The
+// lines live in their own region (RankMem::ll128), never shared with the LL
+// packets: in it the last 16 bytes of a line only ever hold epochs.
+// Also here: the ring allreduce (Alg. 1) on LL128 lines (lane_ring_ll128_kernel)
+// and the lane kernel with Alg. 1 as its inter-node stage (RING2).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
