@@ -1,7 +1,7 @@
 #!/bin/bash
 # busbw vs size for several LANE_* settings (dev tool).
 # usage: tools/sweep_sizes.sh NGPU LAYOUT MAXMIB OUT "ENV"...   (extra bench args in $BENCH_ARGS)
-# prints per size: ours/NCCL-ring[/our Alg.1 ring] and the protocol (l = LL, s = simple)
+# prints per size: ours/NCCL-ring[/our Alg.1 ring] and the protocol (l = LL, L = LL128, s = simple)
 NG=$1; L=$2; MX=$3; OUT=$4; shift 4
 port=29800
 for cfg in "$@"; do
@@ -18,7 +18,7 @@ def cell(r):
         s += f"/{r['lane_ring_alg1_busbw']:.0f}"
     if "approach2_busbw" in r:
         s += f"/a{r['approach2_busbw']:.0f}"
-    return s + r.get("protocol", "?")[0] + ("" if r["verified"] else "!")
+    return s + {"ll128": "L"}.get(r.get("protocol"), r.get("protocol", "?")[0]) + ("" if r["verified"] else "!")
 print(sys.argv[1] or "default", sys.argv[3], " ".join(cell(r) for r in rows) if rows else "NO OUTPUT")
 PY
 done
