@@ -282,7 +282,9 @@ int lane_ll128_plan_query(int nodes, int gpus_per_node, int procs_per_gpu, int64
  * sub-part b of chunk `chunk` in inbox `kind` (1 = L1 phase-1 part from node
  * peer slot, 2 = L2 lane RS slot, 3 = L3 lane AG slot, 4 = L4 phase-3 part
  * from node peer slot; b ignored for 2 / 3) for a call with `chunks` chunks
- * and lines_per_subpart lines per sub-part (lane_ll128.cuh layout128).
+ * and lines_per_subpart lines per sub-part (lane_ll128.cuh layout128); kinds
+ * 5 / 6 = the LL128 ring's RS / AG slot `slot` < nodes*gpus_per_node - 1,
+ * lines_per_subpart = lines per ring part (ring_layout128).
  * Errors: INVALID_ARG (any index out of its range). */
 int lane_ll128_line_query(int nodes, int gpus_per_node, int64_t chunks, int64_t lines_per_subpart, int kind, int slot,
                           int64_t chunk, int b, int64_t line, int64_t* index);

@@ -638,9 +638,6 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     const int64_t rest = pl.ng - p.round_g0;
     p.round_len = rest < RC ? rest : RC;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
-    // lines per RS / AG slot of the LL128 ring (the LL128 lane kernel derives
-    // its layout from p.cap and p.su: lane_ll128.cuh layout128)
-    if (ring128) p.ll_slot_g = p.cap * lane::ll128::lines_of(p.sg);
     p.epoch = ++c->epoch;
     void* args[] = {&p};
     const void* fn;
@@ -1410,7 +1407,13 @@ int lane_ll128_line_query(int nodes, int gpus_per_node, int64_t chunks, int64_t 
   if (!index || N < 1 || G < 1 || chunks < 1 || lines_per_subpart < 1) return LANE_ERR_INVALID_ARG;
   if (chunk < 0 || chunk >= chunks || line < 0 || line >= lines_per_subpart) return LANE_ERR_INVALID_ARG;
   const lane::ll128::Layout128 y = lane::ll128::layout128(G, N, chunks, lines_per_subpart);
+  const lane::ll128::RingLayout128 ry = lane::ll128::ring_layout128(N * G, chunks, lines_per_subpart);
   switch (kind) {
+    case 5:
+    case 6:
+      if (slot < 0 || slot >= N * G - 1) return LANE_ERR_INVALID_ARG;
+      *index = kind == 5 ? ry.rs(slot, chunk, line) : ry.ag(slot, chunk, line);
+      return LANE_OK;
     case 1:
     case 4:
       if (slot < 0 || slot >= G - 1 || b < 0 || b >= N) return LANE_ERR_INVALID_ARG;

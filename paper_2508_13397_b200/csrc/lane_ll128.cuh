@@ -601,8 +601,25 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
 // AG slot s, receive part r-s.
 //
 // Inbox (per parity set): RS slots s = 0..P-2 then AG slots, each
-// p.ll_slot_g = cap * lp lines (lp = ceil(ceil(cg/P)/7) lines per ring part).
+// cap * lp lines (lp = ceil(ceil(cg/P)/7) lines per ring part).
 LANE_HD int64_t ring_set_lines(int P, int64_t cap, int64_t lp) { return 2 * (int64_t)(P - 1) * cap * lp; }
+
+// Line index within a parity set of RS slot s / AG slot s, chunk c, line ln
+// (host and device; tiled exactly, checked on CPU via lane_ll128_line_query).
+struct RingLayout128 {
+  int64_t slot, lp;  // lines per slot (cap * lp), lines per ring part
+  int P;
+  LANE_HD int64_t rs(int s, int64_t c, int64_t ln) const { return (int64_t)s * slot + c * lp + ln; }
+  LANE_HD int64_t ag(int s, int64_t c, int64_t ln) const { return (int64_t)(P - 1 + s) * slot + c * lp + ln; }
+};
+
+LANE_HD RingLayout128 ring_layout128(int P, int64_t cap, int64_t lp) {
+  RingLayout128 y;
+  y.slot = cap * lp;
+  y.lp = lp;
+  y.P = P;
+  return y;
+}
 
 template <int DT, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __grid_constant__ LaneParams p) {
@@ -629,10 +646,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
   const int64_t ncj = nc > j ? (nc - j + p.C - 1) / p.C : 0;  // chunks j, j+C, ... of this CTA
   uint4* const mine = reinterpret_cast<uint4*>(p.rk[r].ll128) + (int64_t)(ep & 1u) * p.ll_set * 8;
   uint4* const next = reinterpret_cast<uint4*>(p.rk[(r + 1) % P].ll128) + (int64_t)(ep & 1u) * p.ll_set * 8;
-  auto rs = [&](uint4* b, int s, int64_t id, int64_t ln) { return b + ((int64_t)s * p.ll_slot_g + id * lp + ln) * 8; };
-  auto ag = [&](uint4* b, int s, int64_t id, int64_t ln) {
-    return b + ((int64_t)(P - 1 + s) * p.ll_slot_g + id * lp + ln) * 8;
-  };
+  const RingLayout128 ry = ring_layout128(P, p.cap, lp);
+  auto rs = [&](uint4* b, int s, int64_t id, int64_t ln) { return b + ry.rs(s, id, ln) * 8; };
+  auto ag = [&](uint4* b, int s, int64_t id, int64_t ln) { return b + ry.ag(s, id, ln) * 8; };
   auto md = [&](int x) { return ((x % P) + P) % P; };
 
   // flat space: (chunk of this CTA, line of a ring part); U lines per group per warp step

@@ -47,13 +47,26 @@ def test_layout_tiles_the_set_exactly(N, G):
         assert sorted(seen) == list(range(2 * G * N * cap * lu)), (N, G, cap, lu)
 
 
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_ring_layout_tiles_the_set_exactly(P):
+    for cap, lp in itertools.product((1, 4), (1, 3)):
+        seen = []
+        for kind in (5, 6):
+            for s, c, ln in itertools.product(range(P - 1), range(cap), range(lp)):
+                code, idx = line(1, P, cap, lp, kind, s, c, 0, ln)
+                assert code == 0
+                seen.append(idx)
+        assert sorted(seen) == list(range(2 * (P - 1) * cap * lp)), (P, cap, lp)
+
+
 def test_line_query_rejects_out_of_range():
     assert line(2, 2, 1, 1, 1, 1, 0, 0, 0)[0] == -1  # G-1 = 1 L1 slot
     assert line(2, 2, 1, 1, 2, 2, 0, 0, 0)[0] == -1  # N = 2 L2 slots
     assert line(2, 2, 2, 3, 3, 0, 2, 0, 0)[0] == -1  # chunk
     assert line(2, 2, 2, 3, 4, 0, 0, 2, 0)[0] == -1  # sub-part
     assert line(2, 2, 2, 3, 4, 0, 0, 0, 3)[0] == -1  # line
-    assert line(2, 2, 2, 3, 5, 0, 0, 0, 0)[0] == -1  # kind
+    assert line(2, 2, 2, 3, 7, 0, 0, 0, 0)[0] == -1  # kind
+    assert line(2, 2, 2, 3, 5, 3, 0, 0, 0)[0] == -1  # ring slot (P - 1 = 3 slots)
 
 
 def _sizes():
