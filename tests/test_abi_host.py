@@ -3,9 +3,11 @@
 - the library loads and exports every function include/lane_allreduce.h declares;
 - the library's own topology and partition (the code the kernels run, via the
   shared lane_plan.h) equal the oracle's, which was written independently;
-- argument validation names the offending field.
+- argument validation names the offending field;
+- the binding fails loudly without the library; the reference arm prints the contract line.
 """
 import ctypes
+import os
 
 import numpy as np
 import pytest
@@ -74,3 +76,33 @@ def test_validation_names_the_field():
         assert field in lib.lane_allreduce_last_error(None).decode()
     assert lib.lane_topology_query(2, 4, 8, None, None, None, None) == -1
     assert lib.lane_partition_query(10, 3, 1, 1, 1, 0, 0, None, 0, None) == -2
+
+
+def test_missing_library_fails_loudly(monkeypatch):
+    """No fallback: without the CUDA library the binding raises (never a CPU path)."""
+    import paper_2508_13397_b200 as lane
+    monkeypatch.setattr(_lib, "LIB_PATH", os.path.join(os.path.dirname(_lib.LIB_PATH), "absent.so"))
+    monkeypatch.setattr(_lib, "_lib", None)
+    with pytest.raises(ImportError):
+        _lib.load()
+    with pytest.raises(ImportError):
+        lane.LaneEmulator(2, 2, 1, device=0)
+
+
+def test_reference_arm_line_n1_cpu():
+    """``bench.py --impl reference`` at N = 1 prints the contract line on CPU."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--steps", "1",
+                        "--warmup", "1"], capture_output=True, text=True, timeout=300, cwd=root, env=env)
+    assert r.returncode == 0, r.stderr[-2000:]
+    d = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
+                "scaling", "vs_baseline", "dtype", "data", "config", "impl", "cpu_baseline", "e2e", "gpu_launches"):
+        assert key in d, key
+    assert d["impl"] == "reference" and d["n_gpus"] == 1 and d["steps"] == 1 and d["warmup"] == 1
+    assert d["unit"] == d["e2e"]["unit"] == "GB/s" and d["higher_is_better"] is True
+    assert d["config"]["layout"] == "2x4" and d["cpu_baseline"]["cores"] >= 1
