@@ -416,18 +416,28 @@ bool overlaps_partially(const void* s, const void* r, uint64_t bytes) {
   return a < b + bytes && b < a + bytes;
 }
 
+// Which kernel a plan launches (Plan::ll).
+enum PlanKind : int {
+  kSimple = 0,      // TMA (or LSU) engine, simple protocol, rounds of LANE_ROUND_BYTES
+  kLL = 1,          // LL lane kernel, one launch (ll_plan)
+  kLaneRingLL = 2,  // LL lane kernel with the ring inter-node stage (rounds, ring_plan)
+  kRingLL = 3,      // flat ring, Alg. 1, on LL packets (rounds, ring_plan)
+  kLL128 = 4,       // LL128 lane kernel, one launch (ll128_plan)
+  kA2LL = 5,        // "approach 2" on LL packets (rounds, a2_plan)
+  kRingLL128 = 6,   // flat ring on LL128 lines (rounds, ring_plan)
+  kLaneRingLL128 = 7  // LL128 lane kernel with the ring inter-node stage (rounds, ring_plan)
+};
+
 struct Plan {
   int64_t ng, cg, round_len0;
   int rounds, C, tail_elems, q;
-  int ll;  // 1: LL lane kernel, one launch; 2: LL lane kernel with the ring
-          // inter-node stage (rounds, ring_plan); 3: flat ring (ring_plan);
-          // 4: LL128 lane kernel, one launch; 5: "approach 2" (rounds, a2_plan);
-          // 6: flat ring on the LL128 protocol (ring_plan); 7: LL128 lane kernel
-          // with the ring inter-node stage (rounds, ring_plan)
+  int ll;  // PlanKind
 };
 
 // Plans whose rounds are LL-capacity sized (ll_ring_rounds launches them).
-bool ll_rounds(const Plan& pl) { return pl.ll == 2 || pl.ll == 3 || pl.ll == 5 || pl.ll == 6 || pl.ll == 7; }
+bool ll_rounds(const Plan& pl) {
+  return pl.ll == kLaneRingLL || pl.ll == kRingLL || pl.ll == kA2LL || pl.ll == kRingLL128 || pl.ll == kLaneRingLL128;
+}
 
 bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl);
 bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl);
@@ -457,7 +467,7 @@ bool ll_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   if (cap * sg > c->ll_slot_g || cap * su > c->ll_slot_u) return false;
   pl->C = C;
   pl->cg = cg;
-  pl->ll = 1;
+  pl->ll = kLL;
   return true;
 }
 
@@ -474,7 +484,7 @@ bool ll128_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   if (g.need > c->ll128_set) return false;
   pl->C = g.C;
   pl->cg = g.cg;
-  pl->ll = 4;
+  pl->ll = kLL128;
   return true;
 }
 
@@ -485,7 +495,7 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   pl->tail_elems = (int)(count - (uint64_t)(pl->ng - 1) * pl->q);
   pl->round_len0 = pl->ng < c->round_cap ? pl->ng : c->round_cap;
   pl->rounds = (int)((pl->ng + c->round_cap - 1) / c->round_cap);
-  pl->ll = 0;
+  pl->ll = kSimple;
   if (c->phase2_ring && c->P > 1) {  // the lane method with a ring inter-node stage: LL rounds only
     if (!ring_plan(c, pl->ng, true, pl))
       return fail(c, LANE_ERR_INVALID_ARG, "LANE_PHASE2=ring: CTA capacity or LL inboxes exceeded");
@@ -573,7 +583,7 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
                                            lane::ll128::lines_of(lane::ceil_div(lane::ceil_div(cg, c->G), c->N)))
                   : lane::ll128::ring_set_lines(c->P, cap, lane::ll128::lines_of(lane::ceil_div(cg, c->P)));
     if (need <= c->ll128_set) {
-      pl->ll = lane_ring ? 7 : 6;
+      pl->ll = lane_ring ? kLaneRingLL128 : kRingLL128;
       return true;
     }
   }
@@ -583,7 +593,7 @@ bool ring_plan(lane_comm_t c, int64_t ng, bool lane_ring, Plan* pl) {
   } else if (cap * lane::ceil_div(cg, c->P) > c->ring_slot) {
     return false;
   }
-  pl->ll = lane_ring ? 2 : 3;
+  pl->ll = lane_ring ? kLaneRingLL : kRingLL;
   return true;
 }
 
@@ -611,21 +621,21 @@ bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   pl->cg = cg;
   pl->rounds = (int)lane::ceil_div(ng, RC);
   pl->round_len0 = r0;
-  pl->ll = 5;
+  pl->ll = kA2LL;
   return true;
 }
 
-// Launch the rounds of a ring_plan: lane_ring_ll_kernel (flat ring, ll == 3)
-// or lane_ll_kernel with the ring inter-node stage (ll == 2); or of an
-// a2_plan (ll == 5).
+// Launch the rounds of a ring_plan (kRingLL, kLaneRingLL, kRingLL128,
+// kLaneRingLL128) or of an a2_plan (kA2LL).
 int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
   const int ranks_here = c->emulated ? c->P : 1;
-  const bool flat = pl.ll == 3, a2 = pl.ll == 5, ring128 = pl.ll == 6, lane128 = pl.ll == 7;
+  const bool flat = pl.ll == kRingLL, a2 = pl.ll == kA2LL, ring128 = pl.ll == kRingLL128,
+             lane128 = pl.ll == kLaneRingLL128;
   const int64_t RC = c->ll_max;
   p.ll_slot_g = flat ? c->ring_slot : c->ll_slot_g;
   p.ll_slot_u = flat ? 0 : (a2 ? c->a2_slot_v : c->ll_slot_u);
   p.ll_set = (ring128 || lane128) ? c->ll128_set : c->ll_set;
-  p.ring2 = (pl.ll == 2 || lane128) ? 1 : 0;
+  p.ring2 = (pl.ll == kLaneRingLL || lane128) ? 1 : 0;
   p.handshake = 0;
   p.direct = 0;
   p.C = pl.C;
@@ -682,11 +692,11 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.round_len = rest < c->round_cap ? rest : c->round_cap;
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
     // the simple protocol's flag arrays hold chunk_cap chunks (the LL plan checked its inboxes itself)
-    if (!pl.ll && p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
+    if (pl.ll == kSimple && p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
-    if (pl.ll == 4) {  // LL128 protocol: one launch, no scratch flags, no handshake
+    if (pl.ll == kLL128) {  // LL128 protocol: one launch, no scratch flags, no handshake
       p.ll_set = c->ll128_set;  // set stride; the layout follows from p.cap, p.su (layout128)
       p.handshake = 0;
       p.direct = 0;
@@ -705,7 +715,7 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
       if (e != cudaSuccess) return cuda_fail(c, e, "lane_ll128_kernel launch");
       continue;
     }
-    if (pl.ll) {  // LL protocol: one launch, no scratch flags, no handshake
+    if (pl.ll != kSimple) {  // kLL (every other kind returned above): LL protocol, one launch, no scratch flags, no handshake
       p.ll_slot_g = c->ll_slot_g;
       p.ll_slot_u = c->ll_slot_u;
       p.ll_set = c->ll_set;
@@ -1439,7 +1449,7 @@ int lane_allreduce_ring_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype
   pl.ng = (int64_t)((count + q - 1) / q);
   if (!ring_plan(c, pl.ng, false, &pl))
     return fail(c, LANE_ERR_INVALID_ARG, "ring: procs_per_gpu exceeds the co-resident CTA capacity or inboxes");
-  *protocol = pl.ll == 6 ? LANE_PROTO_LL128 : LANE_PROTO_LL;
+  *protocol = pl.ll == kRingLL128 ? LANE_PROTO_LL128 : LANE_PROTO_LL;
   return LANE_OK;
 }
 
@@ -1450,7 +1460,8 @@ int lane_allreduce_protocol(lane_comm_t c, size_t count, lane_dtype_t dtype, int
   Plan pl;
   int st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
-  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : ((pl.ll == 4 || pl.ll == 7) ? LANE_PROTO_LL128 : (pl.ll ? LANE_PROTO_LL : LANE_PROTO_SIMPLE));
+  *protocol = (count == 0 || c->P == 1) ? LANE_PROTO_SIMPLE : ((pl.ll == kLL128 || pl.ll == kLaneRingLL128) ? LANE_PROTO_LL128
+                                                                  : (pl.ll != kSimple ? LANE_PROTO_LL : LANE_PROTO_SIMPLE));
   return LANE_OK;
 }
 
