@@ -241,49 +241,102 @@ def cpu_baseline(N, G, k, dtype, seconds):
                       f"{reps} reps in {el:.1f}s, {t * 1e3:.1f} ms per oracle allreduce (numpy, 1 thread)"}
 
 
+# ----------------------------------------------------------------- in-run verification
+# bench.py checks its own outputs without the oracle (only the cpu_baseline leg
+# and the reference arm run oracle/): the plain definition of the sum, and the
+# canonical reduction order written out here for sampled positions.
+TOLERANCE = {"float32": 1e-6, "bfloat16": 1e-2}  # north_star, relative to sum |x| (DESIGN R#10)
+
+
+def _f32(a, dtype):
+    """Stored values -> float32 (bf16 bits widened exactly)."""
+    import numpy as np
+    if dtype == "bfloat16":
+        return (np.asarray(a, np.uint16).astype(np.uint32) << np.uint32(16)).view(np.float32)
+    return np.asarray(a, np.float32)
+
+
+def _bf16_rne(f):
+    """float32 -> bf16 bits, round to nearest even (finite values)."""
+    import numpy as np
+    u = np.asarray(f, np.float32).view(np.uint32).astype(np.uint64)
+    return ((u + 0x7FFF + ((u >> 16) & 1)) >> 16).astype(np.uint16)
+
+
+def canonical_lane_sum(xs, N, G, dtype):
+    """The lane method's result in its canonical order (DESIGN R#7, R#8): node
+    sums over h = 0..G-1 in order (fp32 accumulate, bf16 rounded once), then
+    the sum of the N node sums over a = 0..N-1 in order (rounded once); int32
+    wraps mod 2^32. xs[p] = rank p's values at the sampled positions."""
+    import numpy as np
+    if dtype == "int32":
+        s = np.zeros(len(xs[0]), np.int64)
+        for x in xs:
+            s += np.asarray(x, np.int64)
+        return (s & 0xFFFFFFFF).astype(np.uint32).view(np.int32)
+    node = []
+    for a in range(N):
+        acc = _f32(xs[a * G], dtype).copy()
+        for h in range(1, G):
+            acc = (acc + _f32(xs[a * G + h], dtype)).astype(np.float32)
+        node.append(_f32(_bf16_rne(acc), dtype) if dtype == "bfloat16" else acc)
+    acc = node[0].copy()
+    for a in range(1, N):
+        acc = (acc + node[a]).astype(np.float32)
+    return _bf16_rne(acc) if dtype == "bfloat16" else acc
+
+
+def _within_tolerance(got, xs, dtype, tol):
+    """int32: exact plain sum mod 2^32; fp: |got - sum| <= tol * sum |x| (float64)."""
+    import numpy as np
+    if dtype == "int32":
+        return np.array_equal(np.asarray(got, np.int32), canonical_lane_sum(xs, 1, len(xs), dtype))
+    ref = np.zeros(len(xs[0]), np.float64)
+    mag = np.zeros(len(xs[0]), np.float64)
+    for x in xs:
+        v = _f32(x, dtype).astype(np.float64)
+        ref += v
+        mag += np.abs(v)
+    return bool(np.all(np.abs(_f32(got, dtype).astype(np.float64) - ref) <= tol * mag * (1 + 1e-9)))
+
+
+def _host_values(t, dtype):
+    import torch
+    t = t.cpu()
+    return t.view(torch.int16).numpy().view("uint16") if dtype == "bfloat16" else t.numpy()
+
+
 def sample_check(outs, N, G, dtype, n, seed, ranks):
-    """Bit-exact check of sampled outputs against the oracle."""
+    """Sampled outputs bit-exact against the canonical order (canonical_lane_sum).
+    With LANE_PHASE2=ring (DESIGN R#22) an element's ring order depends on its
+    whole chunk, which a sample does not carry: there int32 is checked exactly
+    and fp within the north_star tolerance; the bit-exact ring-variant parity
+    is in tests/."""
     import numpy as np
     import torch
-    import oracle
     import seeded_inputs as si
     idx = si.sample_indices(n, 65537, [n // 2, n // 3, n // 5])
     it = torch.from_numpy(idx).to(outs[0].device)
     xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(N * G)]
-    ref = oracle.lane_allreduce(xs, N, G, 1, dtype).out[0]
+    if os.environ.get("LANE_PHASE2") == "ring" and N > 2:
+        return all(_within_tolerance(_host_values(o[it], dtype), xs, dtype, TOLERANCE.get(dtype, 0.0)) for o in outs)
+    ref = canonical_lane_sum(xs, N, G, dtype)
     vb = np.uint16 if dtype == "bfloat16" else np.uint32
-    for o in outs:
-        t = o[it].cpu()
-        got = (t.view(torch.int16).numpy() if dtype == "bfloat16" else t.view(torch.int32).numpy()).view(vb)
-        if not np.array_equal(got, ref.view(vb)):
-            return False
-    return True
+    return all(np.array_equal(_host_values(o[it], dtype).view(vb), ref.view(vb)) for o in outs)
 
 
 def ring_check(out, P, k, dtype, n, seed, plan):
-    """Check of the ring allreduce's output (Alg. 1 order, per-hop rounding):
-    bit-exact against the ring oracle with the library's chunk plan when the
-    whole message is small enough for the oracle; above that, the first 2^16
-    elements against the plain sum within the per-hop error bound."""
+    """Check of the ring allreduce's output (Alg. 1 order, per-hop rounding) on
+    the first 2^16 elements: int32 exact, fp within the per-hop error bound
+    (P-1 roundings, plus one bf16 rounding per hop). Bit-exact ring parity
+    against the ring oracle is in tests/."""
     import numpy as np
-    import torch
-    import oracle
     import seeded_inputs as si
-    m = min(n, 1 << 16)  # the first m elements: a full prefix when n == m, else an exact int check
+    m = min(n, 1 << 16)
     idx = np.arange(m)
     xs = [si.generate_at(dtype, "signed", seed, p, idx) for p in range(P)]
-    got = out[:m].cpu()
-    got = (got.view(torch.int16).numpy() if dtype == "bfloat16" else got.view(torch.int32).numpy())
-    if m == n:
-        ref = oracle.ring_allreduce(xs, k, dtype, plan["chunk_granules"], plan["round_granules"]).out[0]
-        return np.array_equal(got.view(np.uint16 if dtype == "bfloat16" else np.uint32),
-                              ref.view(np.uint16 if dtype == "bfloat16" else np.uint32))
-    ref = oracle.brute_force_sum(xs, dtype)
-    if dtype == "int32":
-        return np.array_equal(got, ref)
-    err = np.abs(oracle.to_float64(got.view(np.uint16) if dtype == "bfloat16" else got.view(np.float32), dtype) - ref)
     u = 2.0 ** -24 + (2.0 ** -8 if dtype == "bfloat16" else 0.0)
-    return bool(np.all(err <= (P - 1) * u * oracle.abs_sum(xs, dtype) * (1 + 1e-9)))
+    return _within_tolerance(_host_values(out[:m], dtype), xs, dtype, (P - 1) * u)
 
 
 def base_line(args, N_gpus, K, W):
