@@ -1,7 +1,8 @@
-"""Small emulated runs of every kernel for compute-sanitizer (dev tool):
-simple (TMA, LSU-store and bulk-store), LL, ring, lane-ring and approach 2,
+"""Small emulated runs of every kernel for compute-sanitizer (test harness, so it
+lives under tests/ — it checks against oracle/):
+simple (TMA, LSU-store and bulk-store), LL, LL128, ring (LL, LL128) and approach 2,
 2x2 and 1x3 layouts, counts with ragged tails. Exits non-zero on a parity
-failure. compute-sanitizer --tool memcheck python tools/sanitize_small.py
+failure. compute-sanitizer --tool memcheck python tests/sanitize_small.py
 """
 import os
 import sys
@@ -51,6 +52,8 @@ def main():
             ok &= run(N, G, 2, n, "ll", "lane")
             ok &= run(N, G, 2, n, "ll", "ring")
             ok &= run(N, G, 2, n, "ll", "a2")
+            ok &= run(N, G, 2, n, "ll128", "lane")
+            ok &= run(N, G, 2, n, "ll128", "ring")
     sys.exit(0 if ok else 1)
 
 
