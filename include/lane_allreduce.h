@@ -55,7 +55,12 @@ typedef enum {
                                   (resolving an unpublished handle) */
   LANE_ERR_TIMEOUT = -5,       /* a device-side wait exceeded LANE_TIMEOUT_MS in
                                   an earlier call; the comm is unusable (finalize) */
-  LANE_ERR_MISALIGNED = -6     /* a buffer pointer is not 16-byte aligned      */
+  LANE_ERR_MISALIGNED = -6,    /* a buffer pointer is not 16-byte aligned      */
+  LANE_ERR_MISMATCH = -7       /* ranks disagreed on a call in an earlier call:
+                                  zero-copy vs staged (registrations), buffer
+                                  offsets, count or dtype; detected by the start
+                                  handshake before any buffer was touched, the
+                                  comm is unusable (finalize) */
 } lane_status_t;
 
 #define LANE_MAX_RANKS 16         /* N*G; one 8-GPU box uses <= 8                 */
@@ -67,6 +72,12 @@ typedef enum {
  * get_handle; the caller all-gathers the P blobs in rank order (the paper
  * broadcasts IPC handles the same way, P L330) and every rank calls
  * open_peers. Only then may lane_allreduce be called.
+ *
+ * Every LANE_* environment setting that shapes a call's plan (protocol
+ * thresholds and capacities, engine, store mode, chunking, CTA budgets,
+ * zero-copy job set, releasers) is read ONCE at init and carried in the blob;
+ * open_peers rejects ranks whose settings differ (INVALID_ARG naming the
+ * setting), so every rank plans every call identically.
  */
 
 /* Create a comm for (nodes, gpus_per_node, procs_per_gpu) = (N, G, k).
@@ -117,13 +128,23 @@ int lane_allreduce_register_handle(lane_comm_t comm, void* ptr, size_t bytes, vo
                                    size_t* blob_bytes);
 int lane_allreduce_register_open(lane_comm_t comm, const void* all_blobs, size_t blob_bytes,
                                  int* reg_id);
-/* Stop using a registration (local; mappings are released at finalize). */
+/* Stop using a registration (mappings are released at finalize). Call it on
+ * every rank in the same order, like register: a call whose buffers are
+ * zero-copy on one rank and staged on another (or at different offsets, or
+ * in registrations made in a different order) is caught by the start
+ * handshake of the simple protocol (the per-call signature: job set,
+ * registration index and offsets, count, dtype, chunking) and fails with
+ * LANE_ERR_MISMATCH on every rank, never with wrong data or a timeout. */
 int lane_allreduce_deregister(lane_comm_t comm, int reg_id);
 
 /* End-to-end variant on HOST buffers: copies host_send to a library-owned
  * device staging buffer, runs lane_allreduce, copies the result to host_recv,
- * all on stream (pinned host memory gives async copies). The caller
- * synchronizes the stream before reading host_recv. */
+ * all on stream (pinned host memory gives async copies). host_send and
+ * host_recv hold count elements each (the caller guarantees the sizes; the
+ * Python binding checks them). The message is cut into pieces of
+ * $LANE_HOST_PIECE_BYTES (default 64 MiB), each its own allreduce, pipelined
+ * over two staging slots; staging grows on demand and is owned by the comm.
+ * The caller synchronizes the stream before reading host_recv. */
 int lane_allreduce_host(lane_comm_t comm, const void* host_send, void* host_recv, size_t count,
                         lane_dtype_t dtype, lane_op_t op, void* stream);
 
@@ -201,8 +222,9 @@ int lane_allreduce_finalize(lane_comm_t comm);
 /* Human-readable reason for the last error on comm (never NULL). */
 const char* lane_allreduce_last_error(lane_comm_t comm);
 
-/* Poll the device-side error word (set by the wait watchdog). Returns
- * LANE_OK or LANE_ERR_TIMEOUT. Does not synchronize. */
+/* Poll the device-side error word (set by the wait watchdog or the start
+ * handshake). Returns LANE_OK, LANE_ERR_TIMEOUT or LANE_ERR_MISMATCH. Does
+ * not synchronize. */
 int lane_allreduce_check(lane_comm_t comm);
 
 /* Per-CTA stall accounting of the last launch (TMA engine), enabled by

@@ -41,6 +41,28 @@ def _check_dev_tensor(t, device_index: int, what: str):
         raise LaneError(-1, f"{what}: must be contiguous")
 
 
+def _check_host_tensor(t, what: str):
+    if t.is_cuda:
+        raise LaneError(-1, f"{what}: must be a host (CPU) tensor")
+    if not t.is_contiguous():
+        raise LaneError(-1, f"{what}: must be contiguous")
+
+
+def _check_pair(out, inp, op: str, host: bool = False, device_index: int = 0):
+    """The one argument check of every allreduce entry point: op, placement,
+    contiguity, and out matching inp in numel and dtype (the C ABI copies
+    count * itemsize bytes into every output)."""
+    if op != "sum":
+        raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
+    for t, what in ((inp, "inp"), (out, "out")):
+        if host:
+            _check_host_tensor(t, what)
+        else:
+            _check_dev_tensor(t, device_index, what)
+    if out.numel() != inp.numel() or out.dtype != inp.dtype:
+        raise LaneError(-1, "out: must match inp in numel and dtype")
+
+
 def _stream_handle(stream) -> int:
     torch = _torch()
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -172,12 +194,7 @@ class LaneComm(_CommBase):
     def allreduce(self, out, inp, op: str = "sum", stream=None):
         """out[i] = sum over ranks of inp[i]; enqueued on ``stream`` (default:
         current). ``out is inp`` (same storage) is in-place."""
-        if op != "sum":
-            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
-        _check_dev_tensor(inp, self.device, "inp")
-        _check_dev_tensor(out, self.device, "out")
-        if out.numel() != inp.numel() or out.dtype != inp.dtype:
-            raise LaneError(-1, "out: must match inp in numel and dtype")
+        _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
                                           _dtype_code(inp), 0, _stream_handle(stream))
         _lib.check(code, self._comm)
@@ -187,12 +204,7 @@ class LaneComm(_CommBase):
         """The paper's "standard" ring allreduce (Alg. 1; with k > 1 the
         standard multi-PPG approach): same contract as ``allreduce``, ring
         reduction order with per-hop rounding."""
-        if op != "sum":
-            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
-        _check_dev_tensor(inp, self.device, "inp")
-        _check_dev_tensor(out, self.device, "out")
-        if out.numel() != inp.numel() or out.dtype != inp.dtype:
-            raise LaneError(-1, "out: must match inp in numel and dtype")
+        _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce_ring(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
                                                _dtype_code(inp), 0, _stream_handle(stream))
         _lib.check(code, self._comm)
@@ -201,12 +213,7 @@ class LaneComm(_CommBase):
     def allreduce_approach2(self, out, inp, op: str = "sum", stream=None):
         """The paper's draft "approach 2" (node allreduce, then lane allreduce
         of the whole buffer): same results as ``allreduce``, more traffic."""
-        if op != "sum":
-            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
-        _check_dev_tensor(inp, self.device, "inp")
-        _check_dev_tensor(out, self.device, "out")
-        if out.numel() != inp.numel() or out.dtype != inp.dtype:
-            raise LaneError(-1, "out: must match inp in numel and dtype")
+        _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce_approach2(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
                                                     _dtype_code(inp), 0, _stream_handle(stream))
         _lib.check(code, self._comm)
@@ -233,10 +240,11 @@ class LaneComm(_CommBase):
     def deregister(self, reg_id: int) -> None:
         _lib.check(_lib.load().lane_allreduce_deregister(self._comm, reg_id), self._comm)
 
-    def allreduce_host(self, out_host, inp_host, stream=None):
+    def allreduce_host(self, out_host, inp_host, op: str = "sum", stream=None):
         """End-to-end allreduce of HOST tensors (H2D, kernels, D2H on one
         stream). Synchronizes the stream before returning."""
         torch = _torch()
+        _check_pair(out_host, inp_host, op, host=True)
         code = _lib.load().lane_allreduce_host(self._comm, inp_host.data_ptr(), out_host.data_ptr(),
                                                inp_host.numel(), _dtype_code(inp_host), 0,
                                                _stream_handle(stream))
@@ -279,53 +287,44 @@ class LaneEmulator(_CommBase):
         for i, t in enumerate(ts):
             if dev:
                 _check_dev_tensor(t, self.device, f"{what}[{i}]")
-            elif t.is_cuda or not t.is_contiguous():
-                raise LaneError(-1, f"{what}[{i}]: must be a contiguous host tensor")
+            else:
+                _check_host_tensor(t, f"{what}[{i}]")
         return (ctypes.c_void_p * self.P)(*[t.data_ptr() for t in ts])
 
-    def allreduce(self, outs, inps, op: str = "sum", stream=None):
+    def _args(self, outs, inps, op, dev=True):
+        """Checks shared by every emulated entry point; returns the ctypes
+        argument tuple (sendbufs, recvbufs, count, dtype)."""
         if op != "sum":
             raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
         n = inps[0].numel()
         if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
             raise LaneError(-1, "all tensors must have the same numel and dtype")
-        code = _lib.load().lane_allreduce_emulated(self._comm, self._ptrs(inps, "inps"), self._ptrs(outs, "outs"),
-                                                   n, _dtype_code(inps[0]), 0, _stream_handle(stream))
+        return self._ptrs(inps, "inps", dev), self._ptrs(outs, "outs", dev), n, _dtype_code(inps[0])
+
+    def allreduce(self, outs, inps, op: str = "sum", stream=None):
+        code = _lib.load().lane_allreduce_emulated(self._comm, *self._args(outs, inps, op), 0,
+                                                   _stream_handle(stream))
         _lib.check(code, self._comm)
         return outs
 
     def allreduce_ring(self, outs, inps, op: str = "sum", stream=None):
         """Ring allreduce (Alg. 1) of all emulated ranks."""
-        if op != "sum":
-            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
-        n = inps[0].numel()
-        if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
-            raise LaneError(-1, "all tensors must have the same numel and dtype")
-        code = _lib.load().lane_allreduce_ring_emulated(self._comm, self._ptrs(inps, "inps"),
-                                                        self._ptrs(outs, "outs"), n, _dtype_code(inps[0]), 0,
+        code = _lib.load().lane_allreduce_ring_emulated(self._comm, *self._args(outs, inps, op), 0,
                                                         _stream_handle(stream))
         _lib.check(code, self._comm)
         return outs
 
     def allreduce_approach2(self, outs, inps, op: str = "sum", stream=None):
         """'Approach 2' (node allreduce, then lane allreduce) of all emulated ranks."""
-        if op != "sum":
-            raise LaneError(-2, "op: only 'sum' (MPI_SUM)")
-        n = inps[0].numel()
-        if any(t.numel() != n or t.dtype != inps[0].dtype for t in list(inps) + list(outs)):
-            raise LaneError(-1, "all tensors must have the same numel and dtype")
-        code = _lib.load().lane_allreduce_approach2_emulated(self._comm, self._ptrs(inps, "inps"),
-                                                             self._ptrs(outs, "outs"), n, _dtype_code(inps[0]), 0,
+        code = _lib.load().lane_allreduce_approach2_emulated(self._comm, *self._args(outs, inps, op), 0,
                                                              _stream_handle(stream))
         _lib.check(code, self._comm)
         return outs
 
-    def allreduce_host(self, outs_host, inps_host, stream=None):
+    def allreduce_host(self, outs_host, inps_host, op: str = "sum", stream=None):
         torch = _torch()
-        n = inps_host[0].numel()
-        code = _lib.load().lane_allreduce_emulated_host(
-            self._comm, self._ptrs(inps_host, "inps", dev=False), self._ptrs(outs_host, "outs", dev=False), n,
-            _dtype_code(inps_host[0]), 0, _stream_handle(stream))
+        code = _lib.load().lane_allreduce_emulated_host(self._comm, *self._args(outs_host, inps_host, op, dev=False),
+                                                        0, _stream_handle(stream))
         _lib.check(code, self._comm)
         (stream or torch.cuda.current_stream()).synchronize()
         return outs_host

@@ -17,7 +17,8 @@ HEADER = os.path.join(ROOT, "include", "lane_allreduce.h")
 
 LANE_OK = 0
 STATUS = {0: "LANE_OK", -1: "LANE_ERR_INVALID_ARG", -2: "LANE_ERR_UNSUPPORTED", -3: "LANE_ERR_CUDA",
-          -4: "LANE_ERR_NOT_CONNECTED", -5: "LANE_ERR_TIMEOUT", -6: "LANE_ERR_MISALIGNED"}
+          -4: "LANE_ERR_NOT_CONNECTED", -5: "LANE_ERR_TIMEOUT", -6: "LANE_ERR_MISALIGNED",
+          -7: "LANE_ERR_MISMATCH"}
 DTYPE = {"int32": 0, "float32": 1, "bfloat16": 2}
 HANDLE_BYTES = 256
 MAX_RANKS = 16

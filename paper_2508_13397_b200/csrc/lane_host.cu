@@ -34,7 +34,23 @@ using lane::Span;
 namespace {
 
 constexpr uint32_t kMagic = 0x4C414E45u;  // "LANE"
-constexpr int kVersion = 1;
+constexpr int kVersion = 2;
+
+// Every setting that shapes a call's plan, read once at init (lane_comm_s::set)
+// and carried in the blob: open_peers rejects ranks whose values differ.
+enum SettingId {
+  kSetEngine, kSetStoreMode, kSetThreads, kSetCtasPerGroup, kSetCgMax, kSetCgMin, kSetChunksPerCta,
+  kSetProto, kSetLL128Max, kSetLL128Lo, kSetLL128Hi, kSetLL128CgMin, kSetLL128U1Max, kSetLLMax,
+  kSetLLThresh, kSetLLCgMin, kSetLLCtas, kSetBulkMin, kSetRingCg, kSetPhase2Ring, kSetDirect,
+  kSetCtasTotal, kSetReleasers, kNumSettings
+};
+const char* const kSettingNames[kNumSettings] = {
+    "LANE_ENGINE", "LANE_STORE", "LANE_THREADS", "LANE_CTAS_PER_GROUP", "LANE_CHUNK_BYTES",
+    "LANE_MIN_CHUNK_BYTES", "LANE_CHUNKS_PER_CTA", "LANE_PROTO", "LANE_LL128_MAX_BYTES",
+    "LANE_LL128_MIN_BYTES", "LANE_LL128_THRESHOLD_BYTES", "LANE_LL128_MIN_CHUNK_BYTES",
+    "LANE_LL128_U1_MAX_BYTES", "LANE_LL_MAX_BYTES", "LANE_LL_THRESHOLD_BYTES", "LANE_LL_MIN_CHUNK_BYTES",
+    "LANE_LL_CTAS", "LANE_BULK_MIN_BYTES", "LANE_RING_CHUNK_BYTES", "LANE_PHASE2", "LANE_DIRECT",
+    "LANE_CTAS_TOTAL", "LANE_RELEASERS"};
 
 struct Blob {
   uint32_t magic;
@@ -43,8 +59,19 @@ struct Blob {
   uint64_t s1_bytes, s2_bytes, r_bytes, flag_bytes, total_bytes;
   int64_t round_cap, chunk_cap;
   cudaIpcMemHandle_t handle;
+  int32_t settings[kNumSettings];
 };
 static_assert(sizeof(Blob) <= LANE_HANDLE_BYTES, "blob too large");
+
+// FNV-1a over the bytes of 64-bit values: the per-call signature the start handshake
+// compares across ranks (lane_tma.cuh).
+uint32_t fnv_mix(uint32_t h, uint64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (uint32_t)((v >> (8 * i)) & 0xFF);
+    h *= 16777619u;
+  }
+  return h;
+}
 
 int64_t env_i64(const char* name, int64_t dflt) {
   const char* v = getenv(name);
@@ -71,6 +98,12 @@ struct lane_comm_s {
   int64_t round_cap = 0;   // granules of message per round (kernel launch)
   int64_t cg_max = 0, cg_min = 0;
   int chunks_per_cta = 4;
+  int direct_mode = 2;     // LANE_DIRECT: registered multi-GPU job set (2 push, 3 pull-all, 0 staged)
+  int direct_emu = 1;      // LANE_DIRECT in emulated mode (1 direct-pull default)
+  bool emu_handshake = false;  // LANE_EMU_HANDSHAKE=1 (tests): start/end handshake in emulated mode
+  int sig_skew = -1;       // LANE_EMU_SIG_SKEW_RANK (tests): that emulated rank publishes a wrong signature
+  int ctas_total = 0;      // LANE_CTAS_TOTAL: simple-protocol CTAs per GPU (multi-GPU)
+  int releasers = 4;       // LANE_RELEASERS (1..4)
   int64_t chunk_cap = 0;   // max chunks per round (flag capacity per flag type)
   uint64_t s1_bytes = 0, s2_bytes = 0, r_bytes = 0, flag_bytes = 0, total_bytes = 0;
   // LL protocol (lane_ll.cuh): message capacity, minimum chunk, inbox geometry
@@ -123,6 +156,7 @@ struct lane_comm_s {
               ev_d[2] = {nullptr, nullptr};
   uint64_t stage_bytes = 0;
   std::string last_error;
+  int32_t settings[kNumSettings];  // plan-shaping settings (Blob::settings)
 };
 
 namespace {
@@ -168,8 +202,8 @@ void size_scratch(lane_comm_t c) {
   c->s1_bytes = (uint64_t)((G - 1) * slot_g) * 16;
   c->s2_bytes = (uint64_t)(N * slot_u) * 16;
   c->r_bytes = (uint64_t)slot_g * 16;
-  c->ctl = (2 * G + 2 * N) * c->chunk_cap;  // enter[P], done[P], counter follow the chunk flags
-  c->flag_bytes = (uint64_t)(c->ctl + 2 * LANE_MAX_RANKS + 1) * 4;
+  c->ctl = (2 * G + 2 * N) * c->chunk_cap;  // control words (lane_plan.h kCtl*) follow the chunk flags
+  c->flag_bytes = (uint64_t)(c->ctl + lane::kCtlWords) * 4;
   auto al = [](uint64_t x) { return (x + 4095) & ~(uint64_t)4095; };
   c->s1_bytes = al(c->s1_bytes);
   c->s2_bytes = al(c->s2_bytes);
@@ -318,6 +352,42 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   {
     const char* p2 = getenv("LANE_PHASE2");
     c->phase2_ring = p2 && strcmp(p2, "ring") == 0;
+  }
+  c->direct_mode = (int)env_i64("LANE_DIRECT", 2);
+  if (c->direct_mode != 0 && c->direct_mode != 3) c->direct_mode = 2;  // 1 (pull) exists only emulated
+  c->direct_emu = (int)env_i64("LANE_DIRECT", 1);
+  if (c->direct_emu < 0 || c->direct_emu > 3) c->direct_emu = 1;
+  c->emu_handshake = env_i64("LANE_EMU_HANDSHAKE", 0) != 0;
+  c->sig_skew = emulated ? (int)env_i64("LANE_EMU_SIG_SKEW_RANK", -1) : -1;
+  c->ctas_total = (int)env_i64("LANE_CTAS_TOTAL", 0);
+  c->releasers = (int)env_i64("LANE_RELEASERS", lane::tma::kReleasers);
+  if (c->releasers < 1) c->releasers = 1;
+  if (c->releasers > lane::tma::kReleasers) c->releasers = lane::tma::kReleasers;
+  {
+    int32_t* v = c->settings;
+    v[kSetEngine] = c->engine;
+    v[kSetStoreMode] = c->store_mode;
+    v[kSetThreads] = c->threads;
+    v[kSetCtasPerGroup] = c->ctas_per_group;
+    v[kSetCgMax] = (int32_t)c->cg_max;
+    v[kSetCgMin] = (int32_t)c->cg_min;
+    v[kSetChunksPerCta] = c->chunks_per_cta;
+    v[kSetProto] = c->proto;
+    v[kSetLL128Max] = (int32_t)c->ll128_max;
+    v[kSetLL128Lo] = (int32_t)c->ll128_lo;
+    v[kSetLL128Hi] = (int32_t)c->ll128_hi;
+    v[kSetLL128CgMin] = (int32_t)c->ll128_cg_min;
+    v[kSetLL128U1Max] = (int32_t)c->ll128_u1_max;
+    v[kSetLLMax] = (int32_t)c->ll_max;
+    v[kSetLLThresh] = (int32_t)c->ll_thresh;
+    v[kSetLLCgMin] = (int32_t)c->ll_cg_min;
+    v[kSetLLCtas] = c->ll_ctas;
+    v[kSetBulkMin] = (int32_t)c->bulk_min;
+    v[kSetRingCg] = (int32_t)c->ring_cg;
+    v[kSetPhase2Ring] = c->phase2_ring ? 1 : 0;
+    v[kSetDirect] = c->direct_mode;
+    v[kSetCtasTotal] = c->ctas_total;
+    v[kSetReleasers] = c->releasers;
   }
   size_scratch(c);
 
@@ -507,7 +577,7 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   int ranks_here = c->emulated ? c->P : 1;
   int C = c->ctas_per_group;
   if (C <= 0) {
-    int budget = c->emulated ? c->max_coresident : (int)env_i64("LANE_CTAS_TOTAL", c->sm_count);
+    int budget = c->emulated ? c->max_coresident : (c->ctas_total > 0 ? c->ctas_total : c->sm_count);
     if (budget > c->max_coresident) budget = c->max_coresident;
     C = budget / (ranks_here * c->k);
   }
@@ -524,6 +594,25 @@ int make_plan(lane_comm_t c, uint64_t count, int dtype, Plan* pl) {
   if (cg < c->cg_min) cg = c->cg_min;
   pl->cg = cg;
   return LANE_OK;
+}
+
+// Per-call signature compared by the start handshake (lane_tma.cuh): every
+// rank of a consistent call computes the same value.
+uint32_t call_signature(lane_comm_t c, const Plan& pl, int direct, int reg_s, int reg_r, uint64_t so, uint64_t ro,
+                        int dtype) {
+  uint32_t h = 2166136261u;
+  h = fnv_mix(h, (uint64_t)direct);
+  h = fnv_mix(h, (uint64_t)(int64_t)reg_s);
+  h = fnv_mix(h, (uint64_t)(int64_t)reg_r);
+  h = fnv_mix(h, so);
+  h = fnv_mix(h, ro);
+  h = fnv_mix(h, (uint64_t)pl.ng);
+  h = fnv_mix(h, (uint64_t)pl.tail_elems);
+  h = fnv_mix(h, (uint64_t)dtype);
+  h = fnv_mix(h, (uint64_t)pl.cg);
+  h = fnv_mix(h, (uint64_t)pl.C);
+  h = fnv_mix(h, (uint64_t)c->k);
+  return h;
 }
 
 LaneParams base_params(lane_comm_t c, const Plan& pl) {
@@ -546,7 +635,9 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.abort_flag = c->abort_dev;
   p.trace = c->trace;
   p.ctl = c->ctl;
-  p.releasers = (int)env_i64("LANE_RELEASERS", lane::tma::kReleasers);
+  p.fcap = c->chunk_cap;
+  p.sig_skew = c->sig_skew;
+  p.releasers = c->releasers;
   return p;
 }
 
@@ -760,6 +851,17 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
   return LANE_OK;
 }
 
+// The device-side error word (watchdog timeout, start-handshake mismatch).
+int device_error(lane_comm_t c, const char* when) {
+  const uint32_t w = c->err_host ? *(volatile uint32_t*)c->err_host : 0u;
+  if (w == 0) return LANE_OK;
+  if (w == (uint32_t)(-LANE_ERR_MISMATCH))
+    return fail(c, LANE_ERR_MISMATCH,
+                std::string("comm: ranks disagreed on a call (zero-copy vs staged buffers, registration, offsets, "
+                            "count or dtype)") + when + "; finalize the comm");
+  return fail(c, LANE_ERR_TIMEOUT, std::string("comm: a device-side wait timed out") + when);
+}
+
 int check_call(lane_comm_t c, uint64_t count, int dtype, int op) {
   if (!c) return LANE_ERR_INVALID_ARG;
   if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
@@ -767,8 +869,8 @@ int check_call(lane_comm_t c, uint64_t count, int dtype, int op) {
   if (op != LANE_SUM) return fail(c, LANE_ERR_UNSUPPORTED, "op: only LANE_SUM (MPI_SUM, P L341)");
   if (!c->connected)
     return fail(c, LANE_ERR_NOT_CONNECTED, "comm: lane_allreduce_open_peers has not completed");
-  if (c->err_host && *(volatile uint32_t*)c->err_host)
-    return fail(c, LANE_ERR_TIMEOUT, "comm: a device-side wait timed out in an earlier call");
+  int e = device_error(c, " in an earlier call");
+  if (e != LANE_OK) return e;
   (void)count;
   return LANE_OK;
 }
@@ -834,16 +936,12 @@ struct RegBlob {
 int ensure_stage(lane_comm_t c, uint64_t bytes) {
   const int nbuf = 4 * (c->emulated ? c->P : 1);  // 2 pipeline slots x (send, recv) per rank
   if (c->stage_bytes >= bytes && (int)c->stage.size() == nbuf) return LANE_OK;
-  for (char* p : c->stage) cudaFree(p);
-  if (c->h2d) {
-    cudaStreamDestroy(c->h2d);
-    cudaStreamDestroy(c->d2h);
-    cudaEventDestroy(c->ev_start);
-    for (int i = 0; i < 2; ++i) {
-      cudaEventDestroy(c->ev_h[i]);
-      cudaEventDestroy(c->ev_k[i]);
-      cudaEventDestroy(c->ev_d[i]);
-    }
+  // Growing the staging: the copy streams and events live as long as the comm
+  // (release()); only the buffers are replaced. Earlier calls' copies and
+  // kernels may still use the old buffers: wait for them first.
+  if (!c->stage.empty()) {
+    LANE_CUDA(c, cudaDeviceSynchronize());
+    for (char* p : c->stage) cudaFree(p);
   }
   c->stage.clear();
   c->stage_bytes = 0;
@@ -920,6 +1018,7 @@ int lane_allreduce_get_handle(lane_comm_t c, void* blob, size_t* blob_bytes) {
   b.round_cap = c->round_cap;
   b.chunk_cap = c->chunk_cap;
   b.handle = c->handle;
+  memcpy(b.settings, c->settings, sizeof(b.settings));
   memcpy(blob, &b, sizeof(b));
   *blob_bytes = sizeof(b);
   return LANE_OK;
@@ -940,8 +1039,14 @@ int lane_allreduce_open_peers(lane_comm_t c, const void* all_blobs, size_t blob_
     if (b.rank != p) return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: not in rank order");
     if (b.N != c->N || b.G != c->G || b.k != c->k)
       return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: ranks disagree on (nodes, gpus_per_node, procs_per_gpu)");
+    for (int i = 0; i < kNumSettings; ++i)
+      if (b.settings[i] != c->settings[i])
+        return fail(c, LANE_ERR_INVALID_ARG,
+                    std::string("all_blobs: ranks disagree on ") + kSettingNames[i] + " (rank " + std::to_string(p) +
+                        ": " + std::to_string(b.settings[i]) + ", rank " + std::to_string(c->rank) + ": " +
+                        std::to_string(c->settings[i]) + "; plan-shaping LANE_* settings must match)");
     if (b.total_bytes != c->total_bytes || b.round_cap != c->round_cap || b.chunk_cap != c->chunk_cap)
-      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: ranks disagree on scratch geometry (LANE_* env)");
+      return fail(c, LANE_ERR_INVALID_ARG, "all_blobs: ranks disagree on scratch geometry (LANE_ROUND_BYTES)");
     if (p == c->rank) continue;
     void* ptr = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.handle, cudaIpcMemLazyEnablePeerAccess);
@@ -975,20 +1080,25 @@ int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t cou
   // zero-copy when both buffers are registered (P L330: the user buffer is
   // shared through IPC handles); peers use the same offsets into theirs
   const int rs = find_reg(c, sendbuf, bytes), rr = find_reg(c, recvbuf, bytes);
-  if (c->engine == 1 && rs >= 0 && rr >= 0 && env_i64("LANE_DIRECT", 2)) {
+  uint64_t so = 0, ro = 0;
+  if (c->engine == 1 && rs >= 0 && rr >= 0 && c->direct_mode != 0) {
     const auto& S = c->regs[rs];
     const auto& R = c->regs[rr];
-    const uint64_t so = (uint64_t)(static_cast<const char*>(sendbuf) - S.base);
-    const uint64_t ro = (uint64_t)(static_cast<char*>(recvbuf) - R.base);
+    so = (uint64_t)(static_cast<const char*>(sendbuf) - S.base);
+    ro = (uint64_t)(static_cast<char*>(recvbuf) - R.base);
     for (int q = 0; q < c->P; ++q)
       if (q != c->rank) {
         p.rk[q].send = S.peer[q] + so;
         p.rk[q].recv = R.peer[q] + ro;
       }
-    const int64_t dm = env_i64("LANE_DIRECT", 2);  // push flavour by default on real peers
-    p.direct = dm == 1 ? 1 : (dm == 3 ? 3 : 2);
-    p.handshake = 1;
+    p.direct = c->direct_mode;  // push flavour by default on real peers
   }
+  // The TMA engine's simple protocol always runs the start/end handshake on
+  // real peers: it carries the call signature, so ranks that disagree on the
+  // job set (a buffer registered on one rank only), the registrations or
+  // offsets, the count or the dtype stop with LANE_ERR_MISMATCH.
+  p.handshake = c->engine == 1 ? 1 : 0;
+  p.sig = call_signature(c, pl, p.direct, p.direct ? rs : -1, p.direct ? rr : -1, so, ro, dtype);
   return launch_rounds(c, p, pl, dtype, s);
 }
 
@@ -1015,8 +1125,11 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   p.nlocal = c->P;
   // emulated: every buffer is addressable; pull flavour by default (fewest HBM
   // bytes), LANE_DIRECT=2 runs the push flavour of the multi-GPU path
-  p.direct = c->engine == 1 ? (int)env_i64("LANE_DIRECT", 1) : 0;
-  if (p.direct < 0 || p.direct > 3) p.direct = 1;
+  p.direct = c->engine == 1 ? c->direct_emu : 0;
+  // test switch: the registered calls' start/end handshake (and its call
+  // signature) across the emulated ranks
+  p.handshake = (c->engine == 1 && c->emu_handshake) ? 1 : 0;
+  p.sig = call_signature(c, pl, p.direct, -1, -1, 0, 0, dtype);
   for (int r = 0; r < c->P; ++r) {
     p.rk[r].send = static_cast<const char*>(sendbufs[r]);
     p.rk[r].recv = static_cast<char*>(recvbufs[r]);
@@ -1354,9 +1467,7 @@ int lane_allreduce_trace(lane_comm_t c, uint64_t* out, size_t max_words, size_t*
 
 int lane_allreduce_check(lane_comm_t c) {
   if (!c) return LANE_ERR_INVALID_ARG;
-  if (c->err_host && *(volatile uint32_t*)c->err_host)
-    return fail(c, LANE_ERR_TIMEOUT, "comm: a device-side wait timed out");
-  return LANE_OK;
+  return device_error(c, "");
 }
 
 int lane_allreduce_plan(lane_comm_t c, size_t count, lane_dtype_t dtype, int64_t* chunk_granules,

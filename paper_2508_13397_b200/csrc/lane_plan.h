@@ -83,11 +83,14 @@ struct LaneParams {
   int64_t round_len;    // granules in this round
   int64_t cg;           // chunk granules
   int64_t sg, su;       // slot strides (granules): max group part / sub-part
-  int64_t cap;          // chunk capacity (flag and slot stride in chunks)
+  int64_t cap;          // chunks of this round (slot stride in chunks)
+  int64_t fcap;         // flag stride in chunks: the comm's fixed chunk_cap (never per call)
   uint32_t epoch;       // monotonically increasing per round, never reset
   int direct;           // 1: every rank's send/recv addressable: zero-copy jobs
-  int handshake;        // 1: start/end handshake (registered user buffers on real peers)
-  int64_t ctl;          // flag index of the control words: enter[P], done[P], CTA counter
+  int handshake;        // 1: start/end handshake (every simple-protocol call on real peers)
+  uint32_t sig;         // call signature checked in the start handshake (host: call_signature)
+  int sig_skew;         // test hook (LANE_EMU_SIG_SKEW_RANK): this rank publishes sig ^ 1, else -1
+  int64_t ctl;          // flag index of the control words: enter[P], done[P], CTA counter, sig[P]
   uint64_t timeout_ns;
   uint32_t* err;        // host-mapped error word (LANE_ERR_TIMEOUT on watchdog)
   uint32_t* abort_flag; // device word: set when any wait of this comm timed out
@@ -110,16 +113,35 @@ enum TraceField {
   kTraceWords
 };
 
-// Flag indices inside RankMem::flags.
-LANE_HD int64_t f1_idx(const LaneParams& p, int h, int64_t c) { return (int64_t)h * p.cap + c; }
+// Flag indices inside RankMem::flags: F1[G] F2[N] F3[N] F4[G], each fcap
+// chunks long, fcap = the comm's chunk_cap fixed at init, so one index has
+// ONE meaning (flag type, peer, chunk id) in every call whatever its size.
+//
+// Reuse argument (flags hold epochs that only grow and are never reset): a
+// waiter of call e accepts flag >= e. The flag at index (F, x, c) is written
+// in call e+1 only by the same peer, for the same (F, x, c), and only after
+// that peer finished call e, which needed this rank's contribution to chunk c
+// of call e, which this rank produces only after its own wait on (F, x, c)
+// of call e (per chunk, phases run in order). So a value >= e+1 can only be
+// seen by a waiter of call e that has already passed. With a per-call stride
+// the same index could mean (F2, b, c') in call e+1 while a slow rank still
+// waits on it as (F1, h, c) in call e, and the early e+1 would pass for it.
+// Control words follow at ctl: enter[MAX_RANKS], done[MAX_RANKS], the CTA
+// counter, then sig[MAX_RANKS] (lane_tma.cuh start/end handshake).
+LANE_HD int64_t f1_idx(const LaneParams& p, int h, int64_t c) { return (int64_t)h * p.fcap + c; }
 LANE_HD int64_t f2_idx(const LaneParams& p, int b, int64_t c) {
-  return ((int64_t)p.G + b) * p.cap + c;
+  return ((int64_t)p.G + b) * p.fcap + c;
 }
 LANE_HD int64_t f3_idx(const LaneParams& p, int b, int64_t c) {
-  return ((int64_t)p.G + p.N + b) * p.cap + c;
+  return ((int64_t)p.G + p.N + b) * p.fcap + c;
 }
 LANE_HD int64_t f4_idx(const LaneParams& p, int h, int64_t c) {
-  return ((int64_t)p.G + 2 * p.N + h) * p.cap + c;
+  return ((int64_t)p.G + 2 * p.N + h) * p.fcap + c;
 }
+constexpr int kCtlEnter = 0;
+constexpr int kCtlDone = LANE_MAX_RANKS;
+constexpr int kCtlCounter = 2 * LANE_MAX_RANKS;
+constexpr int kCtlSig = 2 * LANE_MAX_RANKS + 1;
+constexpr int kCtlWords = 3 * LANE_MAX_RANKS + 1;
 
 }  // namespace lane

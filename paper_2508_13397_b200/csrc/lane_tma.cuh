@@ -590,20 +590,20 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     fence_acq_rel_sys();  // every store this CTA made is visible system-wide
     if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStoreReadWait] = ring->fence_ns;
     if (p.handshake) {
-      // end of call (registered user buffers): the last CTA of this rank tells
+      // end of call (every simple-protocol call on real peers): the last CTA of this rank tells
       // every peer "done with your buffers" and waits until every peer is done
       // with ours, so the call completes only when no peer still reads our
       // sendbuf or writes our recvbuf.
-      uint32_t* cnt = x.me->flags + p.ctl + 2 * p.P;
+      uint32_t* cnt = x.me->flags + p.ctl + kCtlCounter;
       uint32_t old;
       asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(cnt) : "memory");
       if ((int)old + 1 == per_rank) {
         atomicExch(cnt, 0u);
         fence_acq_rel_sys();
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + p.P + x.rank, p.epoch);
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlDone + x.rank, p.epoch);
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + p.P + q)) break;
+          if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + kCtlDone + q)) break;
         if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEndAbs] = globaltimer_ns();
       }
     }
@@ -639,15 +639,36 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     int64_t k = 0;  // global tile counter
     bool ok = true;
     if (p.handshake) {
-      // start of call (registered user buffers): a peer's sendbuf is final and
-      // its recvbuf free once its kernel has started (stream order)
+      // start of call: a peer's sendbuf is final and its recvbuf free once its
+      // kernel has started (stream order). The first CTA of each rank also
+      // publishes the call signature (host call_signature: job set, buffer
+      // offsets in the registrations, count, dtype, chunking) before its enter
+      // flag; every CTA compares every peer's with its own, so ranks that
+      // disagree (one zero-copy, one staged; different offsets or counts)
+      // stop here with LANE_ERR_MISMATCH before touching any buffer, instead
+      // of exchanging wrong data or waiting for flags that never come. The
+      // sig slots are rewritten only in the next call, after the end barrier.
+      const uint32_t my_sig = p.sig ^ (x.rank == p.sig_skew ? 1u : 0u);
       if (blockIdx.x % per_rank == 0) {
+        for (int q = 0; q < p.P; ++q)
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlSig + x.rank, my_sig);
         fence_acq_rel_sys();
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + x.rank, p.epoch);
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlEnter + x.rank, p.epoch);
       }
       for (int q = 0; q < p.P && ok; ++q)
-        if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + q)) ok = false;
+        if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + kCtlEnter + q)) ok = false;
+      for (int q = 0; q < p.P && ok; ++q) {
+        if (q == x.rank) continue;
+        uint32_t v;
+        asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.me->flags + p.ctl + kCtlSig + q) : "memory");
+        if (v != my_sig) {
+          atomicExch(p.abort_flag, 1u);
+          *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_MISMATCH);
+          __threadfence_system();
+          ok = false;
+        }
+      }
       if (ok) fence_async_global();
       if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEnterWait] = globaltimer_ns() - t_start;
     }

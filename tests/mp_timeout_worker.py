@@ -2,7 +2,9 @@
 never joins. Rank 0's kernel must give up after LANE_TIMEOUT_MS (the device
 watchdog, include/lane_allreduce.h LANE_ERR_TIMEOUT) instead of hanging, the
 comm must then report LANE_ERR_TIMEOUT on check() and on the next call, and
-both ranks must shut down cleanly. One case per signalling protocol.
+both ranks must shut down cleanly. One case per signalling protocol. Then
+the call-signature cases (mismatch_cases): ranks that disagree on a call end
+with LANE_ERR_MISMATCH instead of a timeout or wrong data.
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tests/mp_timeout_worker.py
 """
@@ -17,6 +19,57 @@ import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
 import paper_2508_13397_b200 as lane  # noqa: E402
+
+
+def mismatch_cases(rank, world, local):
+    """Ranks that disagree on a simple-protocol call (a buffer registered on
+    one rank only; different offsets into the registrations; different
+    counts) must all stop in the start handshake with LANE_ERR_MISMATCH (-7),
+    promptly (the watchdog is 20 s here), and leave the recvbufs untouched."""
+    bad = 0
+    os.environ["LANE_TIMEOUT_MS"] = "20000"
+    os.environ["LANE_PROTO"] = "simple"
+    n = 1 << 20
+    for case in ("registered_on_one_rank", "offsets", "count"):
+        comm = lane.LaneComm(1, world, 1, rank=rank, device=local)
+        rin = torch.ones(n + 64, device="cuda")
+        rout = torch.empty_like(rin)
+        comm.register(rin)
+        comm.register(rout)
+        if case == "registered_on_one_rank":
+            x, y = (rin[:n], rout[:n]) if rank == 0 else (torch.ones(n, device="cuda"), torch.empty(n, device="cuda"))
+        elif case == "offsets":
+            o = 0 if rank == 0 else 16
+            x, y = rin[o:o + n], rout[o:o + n]
+        else:
+            m = n if rank == 0 else n + 4
+            x, y = rin[:m], rout[:m]
+        y.view(torch.int32).fill_(-1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.time()
+        comm.allreduce(y, x)
+        torch.cuda.synchronize()
+        dt = time.time() - t0
+        try:
+            comm.check()
+            print(f"rank {rank} mismatch/{case}: not reported", flush=True)
+            bad += 1
+        except lane.LaneError as e:
+            if e.code != -7:
+                print(f"rank {rank} mismatch/{case}: code {e.code}", flush=True)
+                bad += 1
+        if not bool((y.view(torch.int32) == -1).all()):
+            print(f"rank {rank} mismatch/{case}: recvbuf written", flush=True)
+            bad += 1
+        if dt > 5:
+            print(f"rank {rank} mismatch/{case}: took {dt:.1f}s", flush=True)
+            bad += 1
+        print(f"rank {rank} mismatch/{case}: LANE_ERR_MISMATCH after {dt:.3f}s", flush=True)
+        dist.barrier()
+        comm.close()
+        dist.barrier()
+    return bad
 
 
 def main():
@@ -57,6 +110,7 @@ def main():
         dist.barrier()
         comm.close()
         dist.barrier()
+    bad += mismatch_cases(rank, world, local)
     t = torch.tensor([bad])
     dist.all_reduce(t)
     if rank == 0:

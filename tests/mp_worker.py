@@ -44,12 +44,15 @@ def main():
     os.environ.setdefault("LANE_ROUND_BYTES", str(64 << 20))
     P = world
     counts = [1, 7, 4099, (1 << 20) + 3] if args.quick else [1, 7, 64, 4099, (1 << 20) + 3, (1 << 24) + 1]
-    ks = [1, 4] if args.quick else [1, 2, 4, 8]
+    ks = [1, 4] if args.quick else [1, 2, 4, 8, 16]
     failures = 0
     t0 = time.time()
     maxb = max(counts) * 4
-    for N, G, k, proto in [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
-                           for pr in ("simple", "pull", "ll", "ll128", "ring2", "ring2_128")]:
+    cases = [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
+             for pr in ("simple", "pull", "ll", "ll128", "ring2", "ring2_128")]
+    if args.quick:  # the standard multi-PPG approach at PPG 16 (Alg. 1 per slice, P L431), both protocols
+        cases += [(1, P, 16, "ll"), (1, P, 16, "ll128")]
+    for N, G, k, proto in cases:
         if True:
             # ll / ll128: every call that fits that protocol's inboxes
             os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "ll128": "ll128",
@@ -95,6 +98,7 @@ def main():
                             ref = oracle.brute_force_sum(xs, dtype)
                         else:
                             pl = comm.plan(n, dtype)
+                            assert pl["chunk_granules"] == 4096 and pl["round_granules"] == (16 << 20) // 16, pl
                             ref = oracle.lane_allreduce(xs, N, G, k, dtype, pl["chunk_granules"],
                                                         pl["round_granules"], phase2="ring").out[0]
                     else:
@@ -117,6 +121,8 @@ def main():
                     comm.check()
                     xs = [si.generate(dtype, "signed", 5 + n, p_, n) for p_ in range(P)]
                     pl = comm.plan(n, dtype, algorithm="ring")
+                    # R#21: the ring geometry is fixed by the env, never by the launch
+                    assert pl["chunk_granules"] == 4096 and pl["round_granules"] == (16 << 20) // 16, pl
                     ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
                     if not np.array_equal(bits(to_numpy(out, dtype)), bits(ref)):
                         print(f"rank {rank} FAIL ring {N}x{G} k={k} {dtype} n={n}", flush=True)

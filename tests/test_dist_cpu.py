@@ -136,3 +136,24 @@ def test_reference_arm_under_torchrun_cpu():
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
     assert d["cpu_baseline"]["kind"] == "oracle" and d["e2e"]["h2d_bytes_per_step"] == 0
     assert d["config"]["layout"] == "2x1"
+
+
+@pytest.mark.parametrize("gpus", [2, 4])
+def test_bench_self_launch_without_torchrun_cpu(gpus):
+    """``python bench.py --gpus N`` WITHOUT torchrun (no RANK / WORLD_SIZE):
+    bench.py launches the N ranks itself through torch.distributed.run on
+    127.0.0.1 and relays rank 0's single JSON line (the --dry-run path does
+    the rendezvous and the max-over-ranks reduction without a GPU)."""
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK", "MASTER_ADDR",
+                                                            "MASTER_PORT")}
+    env["OMP_NUM_THREADS"] = "1"
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", str(gpus), "--dry-run", "--steps", "2",
+           "--warmup", "3"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT, env=env)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.strip()]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == gpus and d["dry_run"] and d["ms_per_step"] == float(gpus)  # max over ranks of 1 + rank
+    assert d["launcher"].startswith("bench.py self-launch")
+    assert d["config"]["layout"] == f"2x{gpus // 2}"

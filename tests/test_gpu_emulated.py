@@ -47,7 +47,8 @@ def emu(N, G, k):
                                                         "LANE_LL_THRESHOLD_BYTES", "LANE_LL_CTAS",
                                                         "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES",
                                                         "LANE_LL128_MIN_BYTES", "LANE_LL128_THRESHOLD_BYTES",
-                                                        "LANE_LL128_MAX_BYTES"))
+                                                        "LANE_LL128_MAX_BYTES", "LANE_DIRECT", "LANE_STORE",
+                                                        "LANE_EMU_HANDSHAKE", "LANE_BULK_MIN_BYTES"))
     if key not in _COMMS:
         while len(_COMMS) >= 4:  # every emulated comm holds P ranks' scratch: keep a few
             _COMMS.pop(next(iter(_COMMS))).close()
@@ -81,20 +82,33 @@ def test_seeded_fill_device_matches_numpy():
             assert np.array_equal(bits(to_numpy(t, dtype)), bits(ref)), (dtype, dist)
 
 
-@pytest.mark.parametrize("N,G", LAYOUTS)
-@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128"])
-def test_parity_layouts(N, G, dtype, mode, monkeypatch):
-    """Simple protocol job sets — LANE_DIRECT 1 = direct-pull (emulated
-    default), 2 = direct-push (the registered multi-GPU job set), 3 = pull-all
-    (registered, every job writes only its own rank's memory), 0 = staged
-    (the unregistered job set) — and the LL and LL128 protocols (lane_ll.cuh,
-    lane_ll128.cuh)."""
+def set_mode(mode, monkeypatch):
+    """Simple-protocol job sets by LANE_DIRECT digit — 1 = direct-pull
+    (emulated default), 2 = direct-push (the registered multi-GPU job set),
+    3 = pull-all (registered, every job writes only its own rank's memory),
+    0 = staged (the unregistered job set) — with suffix 'b' = TMA bulk stores
+    (LANE_STORE=bulk: what every multi-GPU call >= LANE_BULK_MIN_BYTES runs)
+    and 'h' = the start/end handshake with the call signature that every
+    multi-GPU simple-protocol call runs (LANE_EMU_HANDSHAKE=1); or the LL /
+    LL128 protocols."""
     if mode in ("ll", "ll128"):
         monkeypatch.setenv("LANE_PROTO", mode)
-    else:
-        monkeypatch.setenv("LANE_PROTO", "simple")
-        monkeypatch.setenv("LANE_DIRECT", mode)
+        return
+    monkeypatch.setenv("LANE_PROTO", "simple")
+    monkeypatch.setenv("LANE_DIRECT", mode[0])
+    if "b" in mode:
+        monkeypatch.setenv("LANE_STORE", "bulk")
+    if "h" in mode:
+        monkeypatch.setenv("LANE_EMU_HANDSHAKE", "1")
+
+
+@pytest.mark.parametrize("N,G", LAYOUTS)
+@pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "0hb", "2hb", "3hb", "2h", "1b"])
+def test_parity_layouts(N, G, dtype, mode, monkeypatch):
+    """Every job set / store mode / protocol (set_mode) on every layout, k and
+    ragged count, bit-exact vs the oracle."""
+    set_mode(mode, monkeypatch)
     for k in (1, 2, 4):
         for n in COUNTS:
             if mode in ("ll", "ll128"):
@@ -113,19 +127,18 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "mixed"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "mixed", "0hb", "2hb", "3hb"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
-    """Repeated calls reuse scratch, flags and (LL, LL128) the two inbox parity
-    sets; "mixed" alternates the LL, LL128 and simple protocols between calls."""
-    if mode in ("ll", "ll128"):
-        monkeypatch.setenv("LANE_PROTO", mode)
-    elif mode == "mixed":
+    """Repeated calls of varying sizes reuse scratch, flags (fixed flag stride:
+    one index, one meaning across calls), the handshake's control words and
+    (LL, LL128) the two inbox parity sets; "mixed" alternates the LL, LL128 and
+    simple protocols between calls."""
+    if mode == "mixed":
         monkeypatch.setenv("LANE_LL_THRESHOLD_BYTES", str(64 << 10))
         monkeypatch.setenv("LANE_LL128_MIN_BYTES", str(64 << 10))
         monkeypatch.setenv("LANE_LL128_THRESHOLD_BYTES", str(1 << 20))
     else:
-        monkeypatch.setenv("LANE_PROTO", "simple")
-        monkeypatch.setenv("LANE_DIRECT", mode)
+        set_mode(mode, monkeypatch)
     N, G, k = 2, 4, 2
     for it in range(9):
         n = [5000, 1 << 16, 33, 1 << 20, 4097, 1 << 16, 9, 70001, 3][it]
@@ -291,6 +304,16 @@ def test_full_size_sampled_parity(N, G, k, dtype, n):
             os.environ["LANE_ROUND_BYTES"] = old
 
 
+def assert_ring_geometry(pl, chunk_bytes, round_bytes):
+    """The ring's fp result depends on its pipeline chunk and round (R#21), so
+    before the library's plan is handed to the oracle it must equal what R#21
+    fixes from the environment the test set: chunk = LANE_RING_CHUNK_BYTES,
+    round = LANE_LL_MAX_BYTES (in 16-byte granules). A planner that derived
+    them from the launch configuration would otherwise be mirrored, not caught."""
+    assert pl["chunk_granules"] == chunk_bytes // 16, pl
+    assert pl["round_granules"] == round_bytes // 16, pl
+
+
 def run_ring(N, G, k, dtype, xs, inplace=False):
     import torch
     ins = [to_device(x, dtype, "cuda:0") for x in xs]
@@ -318,6 +341,7 @@ def test_ring_parity(P, dtype, proto, monkeypatch):
             xs = si.generate_all(dtype, "signed", 7 + n, P, n)
             got = run_ring(1, P, k, dtype, xs, inplace=(n % 2 == 1))
             pl = emu(1, P, k).plan(n, dtype, algorithm="ring")
+            assert_ring_geometry(pl, 64 << 10, 16 << 20)  # R#21: fixed by the env, not the launch
             ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
             for p, o in enumerate(got):
                 assert np.array_equal(bits(o), bits(ref)), f"ring P={P} k={k} n={n} rank {p}"
@@ -335,6 +359,7 @@ def test_ring_multi_round_and_interleaved_with_lane(proto, monkeypatch):
         xs = si.generate_all(dtype, "signed", 50 + it, 4, n)
         got = run_ring(N, G, k, dtype, xs)
         pl = emu(N, G, k).plan(n, dtype, algorithm="ring")
+        assert_ring_geometry(pl, 64 << 10, 256 << 10)
         assert pl["launches"] == -(-n * (2 if dtype == "bfloat16" else 4) // (256 << 10))
         ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
         assert all(np.array_equal(bits(o), bits(ref)) for o in got), f"ring it={it}"
@@ -360,6 +385,7 @@ def test_lane_ring_phase2_parity(N, G, dtype, proto, monkeypatch):
             xs = si.generate_all(dtype, "signed", 3 + n, N * G, n)
             got = run(N, G, k, dtype, xs, inplace=(n == 7))
             pl = emu(N, G, k).plan(n, dtype)
+            assert_ring_geometry(pl, 8 << 10, 512 << 10)
             ref = oracle.lane_allreduce(xs, N, G, k, dtype, pl["chunk_granules"], pl["round_granules"],
                                         phase2="ring").out[0]
             for p, o in enumerate(got):
@@ -406,5 +432,92 @@ def test_lsu_engine_parity(N, G, monkeypatch):
                 torch.cuda.synchronize()
                 e.check()
                 assert_parity([to_numpy(o, dtype) for o in outs], xs, N, G, dtype, f"lsu {N}x{G} {dtype} n={n}")
+    finally:
+        e.close()
+
+
+@pytest.mark.parametrize("proto", ["ll", "ll128"])
+@pytest.mark.parametrize("k", [8, 16])
+def test_ring_parity_ppg_8_16(proto, k, monkeypatch):
+    """The paper's standard multi-PPG approach at its largest PPG (Alg. 1 on
+    every k-slice, k up to 16, P L335-354, L431 "up to 16") on 8 emulated
+    ranks (the 8-GPU box), both protocols, bit-exact vs the ring oracle."""
+    monkeypatch.setenv("LANE_PROTO", proto)
+    P = 8
+    for dtype in ("float32", "bfloat16", "int32"):
+        for n in (7, 4099, (1 << 18) + 5, (1 << 20) + 3):
+            assert emu(1, P, k).ring_protocol(n, dtype) == proto
+            xs = si.generate_all(dtype, "signed", 70 + n + k, P, n)
+            got = run_ring(1, P, k, dtype, xs)
+            pl = emu(1, P, k).plan(n, dtype, algorithm="ring")
+            assert_ring_geometry(pl, 64 << 10, 16 << 20)
+            ref = oracle.ring_allreduce(xs, k, dtype, pl["chunk_granules"], pl["round_granules"]).out[0]
+            for p, o in enumerate(got):
+                assert np.array_equal(bits(o), bits(ref)), f"ring P=8 k={k} {dtype} n={n} rank {p}"
+
+
+@pytest.mark.parametrize("mode", ["1", "0hb", "2hb", "3hb", "2h"])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_whole_buffer_16mib_job_sets(mode, dtype, monkeypatch):
+    """Every simple-protocol job set at 16 MiB per rank + a ragged tail (the
+    size where the multi-GPU path switches to TMA bulk stores; default
+    chunking, several chunks per CTA), 2x4, k = 2: EVERY element of every
+    rank compared with the oracle (not sampled)."""
+    monkeypatch.setenv("LANE_ROUND_BYTES", str(1 << 30))
+    set_mode(mode, monkeypatch)
+    N, G, k = 2, 4, 2
+    n = (16 << 20) // (2 if dtype == "bfloat16" else 4) + 3
+    xs = si.generate_all(dtype, "signed", 1600 + len(mode), N * G, n)
+    e = emu(N, G, k)
+    assert e.protocol(n, dtype) == "simple"
+    assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"16 MiB whole buffer mode={mode}")
+
+
+def test_handshake_signature_agrees_across_calls(monkeypatch):
+    """LANE_EMU_HANDSHAKE=1: the start handshake compares every rank's call
+    signature; in a consistent call they agree (no LANE_ERR_MISMATCH) across
+    sizes, dtypes and in-place calls, and the comm stays usable."""
+    set_mode("2hb", monkeypatch)
+    N, G, k = 4, 2, 1
+    for it, n in enumerate([1 << 20, 33, (1 << 19) + 7, 1 << 20]):
+        dtype = ["float32", "bfloat16", "int32", "float32"][it]
+        xs = si.generate_all(dtype, "signed", 900 + it, N * G, n)
+        assert_parity(run(N, G, k, dtype, xs, inplace=bool(it % 2)), xs, N, G, dtype, f"handshake it={it}")
+    emu(N, G, k).check()
+
+
+@pytest.mark.parametrize("mode", ["0hb", "2hb", "1h"])
+def test_handshake_signature_mismatch_is_caught(mode, monkeypatch):
+    """A call on which one rank disagrees (test hook LANE_EMU_SIG_SKEW_RANK:
+    that rank publishes a different call signature, as a rank with unregistered
+    buffers or other offsets would) stops in the start handshake on EVERY rank
+    with LANE_ERR_MISMATCH — promptly (far below the 20 s watchdog), before any
+    recvbuf is written — and the comm then refuses further calls."""
+    import time
+    import torch
+    import paper_2508_13397_b200 as lane
+    set_mode(mode, monkeypatch)
+    monkeypatch.setenv("LANE_EMU_HANDSHAKE", "1")
+    monkeypatch.setenv("LANE_EMU_SIG_SKEW_RANK", "3")
+    monkeypatch.setenv("LANE_TIMEOUT_MS", "20000")
+    N, G, n = 2, 4, (1 << 20) + 5
+    e = lane.LaneEmulator(N, G, 2, device=0)  # not cached: the comm is poisoned afterwards
+    try:
+        xs = si.generate_all("float32", "signed", 5, N * G, n)
+        ins = [to_device(x, "float32", "cuda:0") for x in xs]
+        outs = [torch.full_like(t, 0).view(torch.int32).fill_(-1).view(torch.float32) for t in ins]
+        t0 = time.time()
+        e.allreduce(outs, ins)
+        torch.cuda.synchronize()
+        dt = time.time() - t0
+        assert dt < 5.0, f"mismatch took {dt:.1f}s (watchdog instead of the signature check?)"
+        with pytest.raises(lane.LaneError) as ei:
+            e.check()
+        assert ei.value.code == -7
+        with pytest.raises(lane.LaneError) as ei:
+            e.allreduce(outs, ins)
+        assert ei.value.code == -7
+        for o in outs:  # no recvbuf was touched
+            assert bool((o.view(torch.int32) == -1).all())
     finally:
         e.close()
