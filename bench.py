@@ -111,29 +111,81 @@ def busbw(bytes_, P, ms):
 
 
 class Clocks:
-    """nvidia-smi sampler running while the timed region runs."""
+    """SM clock and throttle-reason sampler running while the timed region
+    runs: an NVML thread (5 ms period; the GPU-side work is asynchronous, so
+    the sampling thread only competes with the host's launch loop), or the
+    nvidia-smi CSV loop where NVML is unavailable. __enter__ returns once the
+    first sample is in, so even a short timed region is covered."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpus):
+    def __init__(self, gpus, period=0.005):
         self.gpus = gpus
+        self.period = period
         self.proc = None
+        self.thread = None
+        self.samples = []  # (sm_mhz, max_mhz, reasons)
+        self.source = None
         self.out = os.path.join("/tmp", f"lane_clocks_{os.getpid()}_{id(self)}.csv")
 
+    def _nvml_loop(self, handles, pynvml):
+        bits = {"hw_slowdown": pynvml.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": pynvml.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": pynvml.nvmlClocksEventReasonSwPowerCap}
+        while not self._stop:
+            for h in handles:
+                try:
+                    sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    mx = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    self.samples.append((float(sm), float(mx), {n for n, b in bits.items() if r & b}))
+                except Exception:
+                    pass
+            time.sleep(self.period)
+
     def __enter__(self):
+        import threading
+        self._stop = False
         try:
-            self.f = open(self.out, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
-                 "-i", ",".join(str(g) for g in self.gpus)], stdout=self.f, stderr=subprocess.DEVNULL)
+            import pynvml
+            pynvml.nvmlInit()
+            handles = [pynvml.nvmlDeviceGetHandleByIndex(g) for g in self.gpus]
+            self.thread = threading.Thread(target=self._nvml_loop, args=(handles, pynvml), daemon=True)
+            self.thread.start()
+            self.source = "nvml"
         except Exception:
-            self.proc = None
-        time.sleep(0.3)
+            self.thread = None
+            try:
+                self.f = open(self.out, "w")
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "50",
+                     "-i", ",".join(str(g) for g in self.gpus)], stdout=self.f, stderr=subprocess.DEVNULL)
+                self.source = "nvidia-smi"
+            except Exception:
+                self.proc = None
+        t0 = time.time()
+        while time.time() - t0 < 5.0 and not self._have_sample():
+            time.sleep(0.01)
         return self
 
+    def _have_sample(self):
+        if self.thread is not None:
+            return bool(self.samples)
+        if self.proc is None:
+            return True
+        try:
+            return os.path.getsize(self.out) > 0
+        except OSError:
+            return False
+
     def __exit__(self, *a):
+        self._stop = True
+        if self.thread is not None:
+            self.thread.join()
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
@@ -141,26 +193,31 @@ class Clocks:
 
     def summary(self):
         sm, mx, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        try:
-            for line in open(self.out):
-                f = [x.strip() for x in line.split(",")]
-                if len(f) < 8:
-                    continue
-                try:
-                    sm.append(float(f[1]))
-                    mx.append(float(f[2]))
-                except ValueError:
-                    continue
-                for nm, v in zip(names, f[4:8]):
-                    if v.lower().startswith("active"):
-                        reasons.add(nm)
-        except OSError:
-            pass
+        if self.thread is not None:
+            for a, b, r in self.samples:
+                sm.append(a)
+                mx.append(b)
+                reasons |= r
+        else:
+            try:
+                for line in open(self.out):
+                    f = [x.strip() for x in line.split(",")]
+                    if len(f) < 8:
+                        continue
+                    try:
+                        sm.append(float(f[1]))
+                        mx.append(float(f[2]))
+                    except ValueError:
+                        continue
+                    for nm, v in zip(self.NAMES, f[4:8]):
+                        if v.lower().startswith("active"):
+                            reasons.add(nm)
+            except OSError:
+                pass
         if not sm:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0, "source": self.source}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "sm_min_mhz": min(sm),
+                "reasons": sorted(reasons), "samples": len(sm), "source": self.source}
 
 
 def device_time_ms(fn, steps, warmup, stream, barrier=None):

@@ -12,7 +12,9 @@ import re
 
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
-LIB_PATH = os.path.join(PKG, "liblane_allreduce.so")
+# LANE_LIB_PATH: another build of THIS library (A/B measurements of kernel
+# changes on one box); never a different implementation.
+LIB_PATH = os.environ.get("LANE_LIB_PATH") or os.path.join(PKG, "liblane_allreduce.so")
 HEADER = os.path.join(ROOT, "include", "lane_allreduce.h")
 
 LANE_OK = 0

@@ -287,7 +287,10 @@ int occupancy_of(int engine, int threads) {
 template <int DT>
 int ll_occupancy_of() {
   int nb = 0, nr = 0, na = 0;
+  int nb2 = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, lane::ll::lane_ll_kernel<DT>, lane::ll::kThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb2, lane::ll::lane_ll_kernel<DT, true>, lane::ll::kThreads, 0);
+  nb = nb < nb2 ? nb : nb2;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nr, lane::ll::lane_ring_ll_kernel<DT>, lane::ll::kThreads, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&na, lane::ll::lane_a2_ll_kernel<DT>, lane::ll::kThreads, 0);
   nb = nb < nr ? nb : nr;
@@ -413,9 +416,9 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     for (const void* f : {(const void*)lane::ll128::lane_ll128_kernel<0, false, 1>,
                           (const void*)lane::ll128::lane_ll128_kernel<1, false, 1>,
                           (const void*)lane::ll128::lane_ll128_kernel<2, false, 1>,
-                          (const void*)lane::ll128::lane_ll128_kernel<0, true>,
-                          (const void*)lane::ll128::lane_ll128_kernel<1, true>,
-                          (const void*)lane::ll128::lane_ll128_kernel<2, true>}) {
+                          (const void*)lane::ll128::lane_ll128_kernel<0, true, 1>,
+                          (const void*)lane::ll128::lane_ll128_kernel<1, true, 1>,
+                          (const void*)lane::ll128::lane_ll128_kernel<2, true, 1>}) {
       int mr = 0;
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&mr, f, lane::ll128::kThreads, 0);
       lo = lo < mr ? lo : mr;
@@ -743,9 +746,9 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
     void* args[] = {&p};
     const void* fn;
     if (lane128)
-      fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0, true>
-           : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1, true>
-                                   : (const void*)lane::ll128::lane_ll128_kernel<2, true>;
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0, true, 1>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1, true, 1>
+                                   : (const void*)lane::ll128::lane_ll128_kernel<2, true, 1>;
     else if (ring128)
       fn = dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ring_ll128_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ring_ll128_kernel<1>
@@ -758,10 +761,10 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
       fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ring_ll_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ring_ll_kernel<1>
                                    : (const void*)lane::ll::lane_ring_ll_kernel<2>;
-    else
-      fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ll_kernel<0>
-           : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1>
-                                   : (const void*)lane::ll::lane_ll_kernel<2>;
+    else  // kLaneRingLL: the lane kernel with the ring inter-node stage
+      fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ll_kernel<0, true>
+           : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1, true>
+                                   : (const void*)lane::ll::lane_ll_kernel<2, true>;
     const dim3 grid((unsigned)(ranks_here * c->k * pl.C));
     cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
                                 : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);

@@ -142,18 +142,23 @@ struct Ops<2> {
 // Only the message's last granule can be partial (tail_elems < q); only
 // sendbuf reads and recvbuf writes ever touch it (scratch holds whole,
 // zero-padded granules).
+// (fully unrolled over the 8 halfwords with constant register indices: a
+// byte-addressed view of a local uint4 would live on the stack)
 __device__ __forceinline__ uint4 load_partial(const uint4* p, int nbytes) {
-  uint4 v = make_uint4(0, 0, 0, 0);
   const uint16_t* s = reinterpret_cast<const uint16_t*>(p);
-  uint16_t* d = reinterpret_cast<uint16_t*>(&v);
-  for (int i = 0; i < nbytes / 2; ++i) d[i] = s[i];
-  return v;
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (2 * i < nbytes) w[i >> 1] |= (uint32_t)s[i] << (16 * (i & 1));
+  return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
 __device__ __forceinline__ void store_partial(uint4* p, const uint4& v, int nbytes) {
-  const uint16_t* s = reinterpret_cast<const uint16_t*>(&v);
+  const uint32_t w[4] = {v.x, v.y, v.z, v.w};
   uint16_t* d = reinterpret_cast<uint16_t*>(p);
-  for (int i = 0; i < nbytes / 2; ++i) d[i] = s[i];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+    if (2 * i < nbytes) d[i] = (uint16_t)(w[i >> 1] >> (16 * (i & 1)));
 }
 
 struct Msg {
@@ -163,14 +168,20 @@ struct Msg {
   int partial_bytes;
 };
 
+// The message's one partial granule: out of line (cold), so the unrolled
+// halfword code does not compete for registers in the kernels' hot loops;
+// arguments and result travel by value (registers), nothing by reference.
+__device__ __noinline__ uint4 load_partial_cold(const uint4* p, int nbytes) { return load_partial(p, nbytes); }
+__device__ __noinline__ void store_partial_cold(uint4* p, uint4 v, int nbytes) { store_partial(p, v, nbytes); }
+
 __device__ __forceinline__ uint4 load_x(const Msg& m, int64_t gi) {
-  if (gi == m.partial_g) return load_partial(m.send + gi, m.partial_bytes);
+  if (gi == m.partial_g) return load_partial_cold(m.send + gi, m.partial_bytes);
   return ld_cs(m.send + gi);
 }
 
 __device__ __forceinline__ void store_out(const Msg& m, int64_t gi, const uint4& v) {
   if (gi == m.partial_g) {
-    store_partial(m.recv + gi, v, m.partial_bytes);
+    store_partial_cold(m.recv + gi, v, m.partial_bytes);
     return;
   }
   st_cs(m.recv + gi, v);

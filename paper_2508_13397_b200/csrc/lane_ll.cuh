@@ -67,18 +67,31 @@ __device__ __forceinline__ bool ll_try(const uint64_t* line, uint32_t ep, uint4&
          (uint32_t)(d >> 32) == ep;
 }
 
-// Spin until the packet carries this call's epoch; false on timeout/abort.
-__device__ __noinline__ bool ll_wait_slow(const LaneParams& p, const uint64_t* line, uint4& v) {
+// Result of a slow-path wait, returned BY VALUE: an out-parameter reference
+// into a non-inlined function forces the caller's value (and its neighbours
+// in arrays) through the stack (STL/LDL on the hot path).
+struct Got {
+  uint4 v;
+  int ok;
+};
+
+// Spin until the packet carries this call's epoch; ok = 0 on timeout/abort.
+__device__ __noinline__ Got ll_wait_slow(const LaneParams& p, const uint64_t* line) {
   const uint64_t t0 = globaltimer_ns();
+  Got r;
+  r.ok = 0;
   for (uint32_t it = 1;; ++it) {
-    if (ll_try(line, p.epoch, v)) return true;
+    if (ll_try(line, p.epoch, r.v)) {
+      r.ok = 1;
+      return r;
+    }
     if ((it & 255u) == 0) {
-      if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) return false;
+      if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) return r;
       if (globaltimer_ns() - t0 > p.timeout_ns) {
         atomicExch(p.abort_flag, 1u);
         *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_TIMEOUT);
         __threadfence_system();
-        return false;
+        return r;
       }
     }
   }
@@ -86,7 +99,9 @@ __device__ __noinline__ bool ll_wait_slow(const LaneParams& p, const uint64_t* l
 
 __device__ __forceinline__ bool ll_wait(const LaneParams& p, const uint64_t* line, uint4& v) {
   if (ll_try(line, p.epoch, v)) return true;
-  return ll_wait_slow(p, line, v);
+  const Got r = ll_wait_slow(p, line);
+  v = r.v;
+  return r.ok != 0;
 }
 
 // acc = sum over sources s = 0..n-1 in ascending order (the canonical order,
@@ -113,9 +128,9 @@ __device__ __forceinline__ bool ll_sum(const LaneParams& p, int n, int own, cons
         if (s == own) {
           v[u] = own_v;
         } else if (!hit[u]) {
-          uint4 t;  // the slow path's out-parameter; keeps v[] in registers
-          if (!ll_wait_slow(p, line(s), t)) return false;
-          v[u] = t;
+          const Got t = ll_wait_slow(p, line(s));
+          if (!t.ok) return false;
+          v[u] = t.v;
         }
         if (s == 0)
           O::init(acc, v[u]);
@@ -173,17 +188,21 @@ __device__ __forceinline__ Inbox inbox_of(const LaneParams& p, const RankMem& m)
 
 // LANE_TRACE=1: per CTA, the kernel-start time and the time the LAST thread
 // of the CTA finished each phase (A..E), in trace words 0..5 (ns, globaltimer).
+// Per-CTA phase end times (LANE_TRACE=1) in a __shared__ array; holds only
+// the kernel parameters' address and the array's, both re-derivable, so no
+// register stays live across the phases for it (p.trace is re-read at use).
 struct PhaseClock {
+  const LaneParams* p;
   uint64_t* t;  // shared: [0] start, [1..5] phase ends
-  bool on;
   __device__ __forceinline__ void end(int ph) const {
-    if (on) atomicMax(reinterpret_cast<unsigned long long*>(&t[ph]), (unsigned long long)globaltimer_ns());
+    if (p->trace != nullptr)
+      atomicMax(reinterpret_cast<unsigned long long*>(&t[ph]), (unsigned long long)globaltimer_ns());
   }
 };
 
 __device__ __forceinline__ PhaseClock phase_clock_begin(const LaneParams& p, uint64_t* sh) {
-  PhaseClock pc{sh, p.trace != nullptr};
-  if (pc.on) {
+  PhaseClock pc{&p, sh};
+  if (p.trace != nullptr) {
     if (threadIdx.x < 8) sh[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : 0;
     __syncthreads();
   }
@@ -191,12 +210,14 @@ __device__ __forceinline__ PhaseClock phase_clock_begin(const LaneParams& p, uin
 }
 
 __device__ __forceinline__ void phase_clock_flush(const LaneParams& p, const PhaseClock& pc) {
-  if (!pc.on) return;
+  if (p.trace == nullptr) return;
   __syncthreads();
   if (threadIdx.x < 8) p.trace[(size_t)blockIdx.x * kTraceWords + threadIdx.x] = pc.t[threadIdx.x];
 }
 
-template <int DT>
+// RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a
+// separate instantiation so the default kernel keeps its register budget.
+template <int DT, bool RING2 = false>
 __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(const __grid_constant__ LaneParams p) {
   __shared__ uint64_t clk[8];
   const PhaseClock pc = phase_clock_begin(p, clk);
@@ -244,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(c
   }
 
   pc.end(1);
-  if (p.ring2) {
+  if constexpr (RING2) {
     // ---------------- B'/C'/D' (LANE_PHASE2=ring): the inter-node stage is
     // Alg. 1 among the lane members (P L401, L457: "the ring algorithm is
     // used in the inter-node stage"). Ring chunk t = sub-part t of part g;
@@ -367,7 +388,7 @@ __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(c
   }
 
   pc.end(4);
-  }  // !p.ring2
+  }  // !RING2
 
   // ---------------- E: phase-3 allgather receive
   for (int64_t c = j; c < nc; c += p.C) {

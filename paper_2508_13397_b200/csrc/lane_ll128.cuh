@@ -80,16 +80,24 @@ __device__ __forceinline__ bool group_ready(const uint4& v, int sl, uint32_t ep)
 }
 
 // Warp-collective wait: groups with `need` reload their line until it carries
-// the epoch; v holds the line's 16 bytes of this lane. false on timeout/abort
-// (warp-uniform).
-__device__ __noinline__ bool wait_line(const LaneParams& p, const uint4* line, int sl, bool need, uint4& v) {
+// the epoch; v = this lane's 16 bytes of the line as loaded so far. Returns the
+// line (ok = 0 on timeout/abort, warp-uniform) BY VALUE (ll::Got): a reference
+// out-parameter of a non-inlined function put the caller's loaded lines on
+// the stack (STL.128 after every load, profiles/r01_sass_ll128.txt).
+__device__ __noinline__ ll::Got wait_line(const LaneParams& p, const uint4* line, int sl, bool need, uint4 v) {
   const uint64_t t0 = globaltimer_ns();
   bool got = !need;
+  ll::Got res;
+  res.ok = 0;
   for (uint32_t it = 1;; ++it) {
     if (!got) v = line_load(line, sl);
     const bool r = group_ready(v, sl, p.epoch);
     got = got || r;
-    if (__all_sync(kFull, got)) return true;
+    if (__all_sync(kFull, got)) {
+      res.v = v;
+      res.ok = 1;
+      return res;
+    }
     if ((it & 255u) == 0) {
       bool quit = *reinterpret_cast<volatile uint32_t*>(p.abort_flag) != 0;
       if (!quit && globaltimer_ns() - t0 > p.timeout_ns) {
@@ -98,7 +106,10 @@ __device__ __noinline__ bool wait_line(const LaneParams& p, const uint4* line, i
         __threadfence_system();
         quit = true;
       }
-      if (__any_sync(kFull, quit)) return false;
+      if (__any_sync(kFull, quit)) {
+        res.v = v;
+        return res;
+      }
     }
   }
 }
@@ -117,7 +128,7 @@ template <int U>
 struct BatchT {
   bool act[U], dv[U];
   int t[U], b[U];
-  int64_t ln[U], i[U];
+  int32_t ln[U], i[U];  // line in the sub-part, chunk-relative granule (< 2^31: 32-bit, fewer registers)
 };
 
 // Warp-collective: fetch U lines (inactive lines read as zero, never loaded)
@@ -137,8 +148,11 @@ __device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* cons
   if (__all_sync(kFull, all)) return true;
 #pragma unroll
   for (int u = 0; u < U; ++u)
-    if (!__all_sync(kFull, got[u]))
-      if (!wait_line(p, ptr[u], sl, !got[u], v[u])) return false;
+    if (!__all_sync(kFull, got[u])) {
+      const ll::Got w = wait_line(p, ptr[u], sl, !got[u], v[u]);
+      if (!w.ok) return false;
+      v[u] = w.v;
+    }
   return true;
 }
 
@@ -287,14 +301,14 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
         // positions stay far below 2^31 (total <= M/7 + G*N lines): 32-bit division
         const uint32_t v32 = q.act[u] ? (uint32_t)v : 0u, lu32 = (uint32_t)lu;
         const uint32_t r = v32 / lu32;
-        q.ln[u] = v32 - r * lu32;
+        q.ln[u] = (int32_t)(v32 - r * lu32);
         q.b[u] = (int)(r % (uint32_t)NB);
         q.t[u] = (int)(r / (uint32_t)NB);
         const Span up = span(q.t[u], q.b[u]);
         q.act[u] = q.act[u] && q.ln[u] < lines_of(up.len);
         q.i[u] = q.ln[u] * kLineGranules + sl;
         q.dv[u] = q.act[u] && sl < kLineGranules && q.i[u] < up.len;
-        q.i[u] += up.start;  // granule of the span's chunk-relative part
+        q.i[u] += (int32_t)up.start;  // granule of the span's chunk-relative part
       }
       if (!f(q)) return false;
     }

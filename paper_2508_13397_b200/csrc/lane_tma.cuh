@@ -66,8 +66,9 @@ constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
 constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
 constexpr int kJobCacheBytes = 5 * 576;  // producer's next job of every phase
-constexpr int kSmemBytes =
-    kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 256 + kJobCacheBytes;
+constexpr int kProdStateBytes = 192;     // producer's per-phase cursors (ProdState)
+constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 256 +
+                           kJobCacheBytes + kProdStateBytes;
 
 // ------------------------------------------------------------------ PTX
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -444,18 +445,42 @@ struct RelRing {
 };
 static_assert(sizeof(RelRing) + 4 <= 256, "RelRing must fit its smem slot");
 
-// Storer side: publish a completed job's flags to the releasers.
-__device__ __forceinline__ void publish_release(RelRing* ring, RelRec* rel_rec, uint32_t* const* rel, int nrel) {
+// Storer side, in two steps: reserve_release fills the record at the ring's
+// tail (waiting until the releasers retired the slot) straight from the
+// tile descriptor — shared memory to shared memory, no copy of the flag list
+// in registers or on the stack — and commit_release hands it to the
+// releasers. The storer holds at most one reserved record (the bulk-store
+// path holds a job's release until its stores are done).
+__device__ __forceinline__ void reserve_release(RelRing* ring, RelRec* rel_rec, uint32_t* const* rel, int nrel) {
   const int t = ring->tail;
   while (ring->busy[t % kRelSlots]) {
   }
   RelRec& r = rel_rec[t % kRelSlots];
   r.n = nrel;
   for (int i = 0; i < nrel; ++i) r.f[i] = rel[i];
+}
+__device__ __forceinline__ void commit_release(RelRing* ring) {
+  const int t = ring->tail;
   __threadfence_block();
   ring->busy[t % kRelSlots] = 1;
   ring->tail = t + 1;
 }
+__device__ __forceinline__ void publish_release(RelRing* ring, RelRec* rel_rec, uint32_t* const* rel, int nrel) {
+  reserve_release(ring, rel_rec, rel, nrel);
+  commit_release(ring);
+}
+
+// The producer's per-phase cursors, in shared memory: they are indexed by the
+// picked phase (a run-time value), which in registers would be a stack array.
+struct ProdState {
+  int64_t cur[5];  // next chunk (of this CTA) per phase
+  int nj[5];       // jobs per chunk per phase
+  int prev[5];     // previous active phase
+  int sub[5];      // next job within the chunk
+  int wpos[5];     // flags of the cached job already seen set
+  int have[5];     // cached job valid
+};
+static_assert(sizeof(ProdState) <= kProdStateBytes, "ProdState must fit its smem slot");
 
 // Relaxed poll (no per-poll fence); a fence_acquire_sys() after the last
 // observation completes the acquire pattern.
@@ -507,7 +532,8 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
   RelRec* rel_rec = reinterpret_cast<RelRec*>(desc + kStages);
   RelRing* ring = reinterpret_cast<RelRing*>(rel_rec + kRelSlots);
   volatile int* abort_s = reinterpret_cast<volatile int*>(reinterpret_cast<char*>(ring) + sizeof(RelRing));
-  Job* jobs = reinterpret_cast<Job*>(smem + kSmemBytes - kJobCacheBytes);  // producer only
+  Job* jobs = reinterpret_cast<Job*>(smem + kSmemBytes - kJobCacheBytes - kProdStateBytes);  // producer only
+  ProdState* ps = reinterpret_cast<ProdState*>(smem + kSmemBytes - kProdStateBytes);     // producer only
 
   const int per_rank = p.k * p.C;
   Ctx x;
@@ -625,14 +651,20 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     const bool tr = p.trace != nullptr;
     uint64_t tr_flag = 0, tr_empty = 0;
     const uint64_t t_start = tr ? globaltimer_ns() : 0;
-    int nj[5], prev[5], last = -1;
-    int64_t cur[5];
-    int sub[5];
+    int last = -1;
+    int64_t* const cur = ps->cur;
+    int* const nj = ps->nj;
+    int* const prev = ps->prev;
+    int* const sub = ps->sub;
+    int* const wpos = ps->wpos;  // flags of jobs[ph] already seen set
+    int* const have = ps->have;  // jobs[ph] (shared memory): next job of every phase, built once per job
     for (int ph = 0, pa = -1; ph < 5; ++ph) {
       nj[ph] = njobs(x, ph);
       cur[ph] = nj[ph] > 0 ? 0 : m;  // inactive phases are "done"
       sub[ph] = 0;
       prev[ph] = pa;
+      wpos[ph] = 0;
+      have[ph] = 0;
       if (nj[ph] > 0) pa = last = ph;
     }
     const int64_t window = 6;
@@ -674,9 +706,6 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     }
     if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStartAbs] = t_start;
     uint64_t t_idle = 0;
-    // jobs[ph] (shared memory): next job of every phase, built once per job
-    bool have[5] = {false, false, false, false, false};
-    int wpos[5] = {0, 0, 0, 0, 0};  // flags of jobs[ph] already seen set
     while (ok) {
       int pick = -1;
       bool any_left = false;
@@ -687,7 +716,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
         if (ph == 0 && last >= 0 && last != 0 && cur[0] - cur[last] >= window) continue;
         if (!have[ph]) {
           make_job(x, ph, chunk_geo(p, cb, sl, j + cur[ph] * p.C), sub[ph], jobs[ph]);
-          have[ph] = true;
+          have[ph] = 1;
           wpos[ph] = 0;
         }
         const Job& Jc = jobs[ph];
@@ -713,7 +742,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       }
       const Job& J = jobs[pick];
       if (J.nwait) fence_async_global();  // acquired flags ordered before the async-proxy (TMA) reads
-      have[pick] = false;  // J stays valid until the next make_job of this phase
+      have[pick] = 0;  // J stays valid until the next make_job of this phase
       // advance the phase cursor
       if (++sub[pick] == nj[pick]) {
         sub[pick] = 0;
@@ -798,7 +827,9 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
   const int ct = tid - kConsumerTid0;
   const bool storer = ct == 0;
   const bool tr = storer && p.trace != nullptr;
-  uint64_t tr_full = 0, tr_sync = 0, tr_read = 0, tr_flush = 0, tr_ph[5] = {0, 0, 0, 0, 0}, tr_bytes = 0;
+  uint64_t tr_full = 0, tr_sync = 0, tr_read = 0, tr_flush = 0, tr_bytes = 0;
+  // per-phase tile time (trace): five scalars, not an array indexed by the run-time phase (stack)
+  uint64_t tr_pA = 0, tr_pB = 0, tr_pC = 0, tr_pD = 0, tr_pE = 0;
   uint64_t tr_jobs = 0;
   const uint64_t t_start = tr ? globaltimer_ns() : 0;
   int64_t freed = -1;  // bulk mode: highest tile whose stage was returned to the producer
@@ -807,15 +838,14 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
   // one newer group pending), or as soon as the storer would otherwise idle:
   // a held release may be what a peer waits for before it can feed us.
   int64_t committed = 0;  // bulk groups committed by the storer
-  int pend_n = -1;        // nrel of the held job, -1 = none
+  bool pending = false;   // a held job's release is reserved at the ring's tail (reserve_release)
   int64_t pend_g = 0;     // its last group's sequence number
-  uint32_t* pend_f[kMaxSrc];
   auto flush_pending = [&](int64_t newer) {
-    if (pend_n < 0) return;
+    if (!pending) return;
     bulk_wait_upto(newer);
     fence_async_global();  // the async-proxy (bulk) writes before the generic handoff
-    publish_release(ring, rel_rec, pend_f, pend_n);
-    pend_n = -1;
+    commit_release(ring);
+    pending = false;
   };
   for (int64_t k = 0;; ++k) {
     const int s = (int)(k % kStages);
@@ -824,7 +854,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     const uint64_t tf = tr ? globaltimer_ns() : 0;
     bool aborted = false;
     while (!mbar_try_wait(&full[s], par)) {
-      if (!kLsuStore && storer && pend_n >= 0) flush_pending(0);  // do not hold a release while idle
+      if (!kLsuStore && storer && pending) flush_pending(0);  // do not hold a release while idle
       if ((++spins & 1023u) == 0 && *reinterpret_cast<volatile uint32_t*>(p.abort_flag)) {
         aborted = true;
         break;
@@ -886,8 +916,6 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       consumers_sync();
       if (tr) tr_sync += globaltimer_ns() - ts;
       if (storer) {
-        uint32_t* rel[kMaxSrc];
-        for (int r = 0; r < nrel; ++r) rel[r] = d.rel[r];
         for (int dd = 0; dd < ndst; ++dd) {
           uint4* dp = d.dst[dd];
           int64_t cnt = tl;
@@ -902,22 +930,29 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
         const uint64_t tq = tr ? globaltimer_ns() : 0;
         bulk_wait_read1();  // every store group but this tile's has read its smem
         if (tr) tr_read += globaltimer_ns() - tq;
-        if (k >= 1 && k - 1 > freed) {
+        if (k >= 1 && k - 1 > freed) {  // the previous stage (and its descriptor) back to the producer
           mbar_arrive(&empty[(k - 1) % kStages]);
           freed = k - 1;
         }
         const uint64_t tw = tr ? globaltimer_ns() : 0;
         flush_pending(committed - pend_g);  // the held job's groups are older than this tile's
         if (nrel > 0) {  // job complete: hold its release until its bulk stores are done
-          pend_n = nrel;
+          reserve_release(ring, rel_rec, d.rel, nrel);  // this stage's descriptor: freed only at tile k+1
+          pending = true;
           pend_g = committed;
-          for (int r = 0; r < nrel; ++r) pend_f[r] = rel[r];
         }
         if (tr) tr_flush += globaltimer_ns() - tw;
       }
     }
     if (tr) {
-      tr_ph[ph] += globaltimer_ns() - t_tile;
+      const uint64_t dt = globaltimer_ns() - t_tile;
+      switch (ph) {
+        case 0: tr_pA += dt; break;
+        case 1: tr_pB += dt; break;
+        case 2: tr_pC += dt; break;
+        case 3: tr_pD += dt; break;
+        default: tr_pE += dt; break;
+      }
       tr_bytes += (uint64_t)tl * 16 * ndst;
       if (nrel) ++tr_jobs;
     }
@@ -937,7 +972,11 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     Tr[kTrStoreSync] = tr_sync;
     Tr[kTrStoreFlush] = tr_flush;
     Tr[kTrStoreJobs] = tr_jobs;
-    for (int i = 0; i < 5; ++i) Tr[kTrPhaseA + i] = tr_ph[i];
+    Tr[kTrPhaseA] = tr_pA;
+    Tr[kTrPhaseB] = tr_pB;
+    Tr[kTrPhaseC] = tr_pC;
+    Tr[kTrPhaseD] = tr_pD;
+    Tr[kTrPhaseE] = tr_pE;
     Tr[kTrBytes] = tr_bytes;
   }
 }

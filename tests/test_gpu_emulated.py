@@ -521,3 +521,25 @@ def test_handshake_signature_mismatch_is_caught(mode, monkeypatch):
             assert bool((o.view(torch.int32) == -1).all())
     finally:
         e.close()
+
+
+def test_host_api_staging_grows_between_calls(monkeypatch):
+    """lane_allreduce_emulated_host with a small message and then larger ones
+    on the SAME comm: the staging buffers grow while the copy streams and
+    events stay valid (advisor finding: they used to be destroyed and reused)."""
+    import torch
+    import paper_2508_13397_b200 as lane
+    monkeypatch.delenv("LANE_HOST_PIECE_BYTES", raising=False)
+    N, G = 2, 2
+    e = lane.LaneEmulator(N, G, 1, device=0)
+    try:
+        for it, n in enumerate([1000, 300001, (1 << 21) + 3, 5000]):
+            xs = si.generate_all("float32", "signed", 300 + it, N * G, n)
+            ins = [torch.from_numpy(x).pin_memory() for x in xs]
+            outs = [torch.empty_like(t).pin_memory() for t in ins]
+            e.allreduce_host(outs, ins)
+            assert_parity([to_numpy(o, "float32") for o in outs], xs, N, G, "float32", f"host grow n={n}")
+        with pytest.raises(lane.LaneError):
+            e.allreduce_host([torch.empty(10) for _ in range(4)], [torch.empty(11) for _ in range(4)])
+    finally:
+        e.close()
