@@ -1,11 +1,15 @@
-"""Stress (multi-GPU): thousands of back-to-back allreduces on one comm,
-alternating the LL, LL128 and simple protocols, sizes across their thresholds and
-the bulk-store threshold, registered and unregistered buffers, in-place and
-out-of-place — every call checked exactly (int32: the expected sum is a
-closed form, computed on the device with plain torch ops). Looks for rare
-races in epoch / parity-set / scratch reuse that a few calls would not hit.
+"""Stress (multi-GPU): thousands of back-to-back allreduces on one comm per
+virtual layout, alternating the LL, LL128 and simple protocols, sizes across
+their thresholds and the bulk-store threshold, int32 / fp32 / bf16, registered
+and unregistered buffers, in-place and out-of-place — every call checked
+bit-exactly on the device against the canonical-order sum (DESIGN R#7/R#8;
+bench.canonical_lane_sum_torch, pinned to the oracle by the CPU tests) of the
+P seeded inputs regenerated on the device. fp32 / bf16 matter here: an int32
+closed form cannot see a torn LL128 line whose data happen to match (R#25).
+Looks for rare races in epoch / parity-set / scratch reuse that a few calls
+would not hit.
 
-    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_stress_worker.py [--iters N]
+    torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_stress_worker.py [--iters N] [--layouts all|NxG]
 """
 import argparse
 import os
@@ -18,57 +22,81 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import torch.distributed as dist  # noqa: E402
 
+import bench  # noqa: E402
 import paper_2508_13397_b200 as lane  # noqa: E402
+from seeded_inputs import device as sdev  # noqa: E402
+
+TDT = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
+
+
+def stress(N, G, iters, rank, world, local):
+    comm = lane.LaneComm(N, G, 2, rank=rank, device=local)
+    nbytes = 24 << 20
+    rin = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    rout = torch.empty_like(rin)
+    comm.register(rin)
+    comm.register(rout)
+    # bytes per rank: LL (<= 1 MiB), LL128 (1-16 MiB), simple, simple with bulk stores (>= 16 MiB)
+    sizes = [4, 4000, 16396, 1 << 20, (3 << 20) + 20, (8 << 20) + 12, (16 << 20) - 4, (9 << 20) + 68,
+             (20 << 20) + 4, nbytes]
+    g = torch.Generator().manual_seed(1234 + N)  # same sequence on every rank
+    bad = 0
+    for it in range(iters):
+        nb = sizes[int(torch.randint(len(sizes), (1,), generator=g))]
+        dtype = ["int32", "float32", "bfloat16"][int(torch.randint(3, (1,), generator=g))]
+        mode = int(torch.randint(4, (1,), generator=g))  # registered? in place?
+        registered, inplace = mode & 1, mode & 2
+        tdt = TDT[dtype]
+        n = nb // (2 if dtype == "bfloat16" else 4)
+        seed = 5000 + it
+        dist_ = "full" if dtype == "int32" else "signed"
+        inp = rin[:n * tdt.itemsize].view(tdt) if registered else torch.empty(n, dtype=tdt, device="cuda")
+        sdev.fill(inp, dtype, dist_, seed, rank)
+        out = inp if inplace else (rout[:n * tdt.itemsize].view(tdt) if registered else torch.empty_like(inp))
+        comm.allreduce(out, inp)
+        xs = [sdev.fill(torch.empty(n, dtype=tdt, device="cuda"), dtype, dist_, seed, p) for p in range(N * G)]
+        want = bench.canonical_lane_sum_torch(xs, N, G, dtype)
+        if not torch.equal(bench._bitview(out), bench._bitview(want)):
+            bad += 1
+            if bad < 5:
+                print(f"rank {rank} {N}x{G} it {it} {dtype} n={n} mode={mode} proto={comm.protocol(n, dtype)}: "
+                      f"MISMATCH ({int((bench._bitview(out) != bench._bitview(want)).sum())} elements)", flush=True)
+    torch.cuda.synchronize()
+    comm.check()
+    dist.barrier()
+    comm.close()
+    dist.barrier()
+    return bad
 
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--iters", type=int, default=2000)
-    ap.add_argument("--layout", default=None)
+    ap.add_argument("--iters", type=int, default=2000, help="calls per layout")
+    ap.add_argument("--layouts", default="default", help="'all', 'default' (2 x P/2) or NxG")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     os.environ.setdefault("LANE_TIMEOUT_MS", "10000")
-    N, G = map(int, a.layout.split("x")) if a.layout else (2, world // 2) if world % 2 == 0 else (world, 1)
-    comm = lane.LaneComm(N, G, 2, rank=rank, device=local)
-    nmax = (24 << 20) // 4  # 24 MiB of int32
-    rin = torch.empty(nmax, dtype=torch.int32, device="cuda")
-    rout = torch.empty_like(rin)
-    comm.register(rin)
-    comm.register(rout)
-    # LL (<= 1 MiB), LL128 (1-16 MiB), simple, simple with bulk stores (>= 16 MiB)
-    sizes = [1, 1000, 4099, 1 << 18, (3 << 18) + 5, (1 << 21) + 3, (1 << 22) - 1, (2 << 20) + 17, (5 << 20) + 1, nmax]
-    g = torch.Generator().manual_seed(1234)  # same sequence on every rank
-    bad = 0
-    t0 = time.time()
-    for it in range(a.iters):
-        n = sizes[int(torch.randint(len(sizes), (1,), generator=g))]
-        mode = int(torch.randint(4, (1,), generator=g))  # registered? in place?
-        registered, inplace = mode & 1, mode & 2
-        idx = torch.arange(n, device="cuda", dtype=torch.int64)
-        base = (idx * 7 + it) % (1 << 20)
-        inp = rin[:n] if registered else torch.empty(n, dtype=torch.int32, device="cuda")
-        inp.copy_((base + 13 * rank).to(torch.int32))
-        out = inp if inplace else (rout[:n] if registered else torch.empty_like(inp))
-        comm.allreduce(out, inp)
-        want = (base * world + 13 * (world * (world - 1) // 2)).to(torch.int32)
-        if not torch.equal(out, want):
-            bad += 1
-            if bad < 5:
-                print(f"rank {rank} it {it} n={n} mode={mode} proto={comm.protocol(n, 'int32')}: MISMATCH "
-                      f"({int((out != want).sum())} elements)", flush=True)
-    torch.cuda.synchronize()
-    comm.check()
-    t = torch.tensor([bad])
-    dist.all_reduce(t)
-    if rank == 0:
-        print(f"mp_stress_worker P={world} {N}x{G}: {'OK' if t.item() == 0 else 'FAILED'} ({t.item()} bad calls of "
-              f"{a.iters}) in {time.time() - t0:.1f}s", flush=True)
-    comm.close()
+    if a.layouts == "all":
+        layouts = [(N, world // N) for N in range(1, world + 1) if world % N == 0]
+    elif a.layouts == "default":
+        layouts = [(2, world // 2) if world % 2 == 0 else (world, 1)]
+    else:
+        layouts = [tuple(map(int, a.layouts.split("x")))]
+    total = 0
+    for N, G in layouts:
+        t0 = time.time()
+        bad = stress(N, G, a.iters, rank, world, local)
+        t = torch.tensor([bad])
+        dist.all_reduce(t)
+        total += t.item()
+        if rank == 0:
+            print(f"mp_stress_worker P={world} {N}x{G}: {'OK' if t.item() == 0 else 'FAILED'} ({t.item()} bad calls "
+                  f"of {a.iters}, int32/fp32/bf16 bit-exact) in {time.time() - t0:.1f}s", flush=True)
     dist.destroy_process_group()
-    sys.exit(1 if t.item() else 0)
+    sys.exit(1 if total else 0)
 
 
 if __name__ == "__main__":

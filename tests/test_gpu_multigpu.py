@@ -44,16 +44,21 @@ def test_watchdog_timeout_p2():
     assert "mp_timeout_worker: OK" in out, out[-4000:]
 
 
-@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("P", [2, 4, 8])
 def test_stress_back_to_back(P):
-    """1000 back-to-back calls on one comm across the LL / simple / bulk-store
-    thresholds, registered or not, in place or not; every call checked exactly."""
+    """Back-to-back calls on one comm per virtual layout (every layout of P)
+    across the LL / LL128 / simple / bulk-store thresholds, int32 / fp32 / bf16,
+    registered or not, in place or not; every call checked bit-exactly
+    (fp32 / bf16 included: R#25, the LL128 line property, at up to 7 writers
+    per GPU through NVSwitch when P = 8). Budget: P = 4 ran 3 x 400 calls in
+    well under the limit; P = 8 runs 4 layouts x 300."""
     if _ngpus() < P:
         pytest.skip(f"needs {P} GPUs, have {_ngpus()}")
+    iters = {2: 600, 4: 400, 8: 300}[P]
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
            "--master-addr", "127.0.0.1", "--master-port", str(29620 + P),
-           os.path.join(ROOT, "tests", "mp_stress_worker.py"), "--iters", "1000"]
-    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+           os.path.join(ROOT, "tests", "mp_stress_worker.py"), "--iters", str(iters), "--layouts", "all"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=1200, cwd=ROOT)
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "mp_stress_worker" in out and ": OK" in out, out[-4000:]
