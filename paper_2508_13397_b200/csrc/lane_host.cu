@@ -98,7 +98,7 @@ struct lane_comm_s {
   int64_t round_cap = 0;   // granules of message per round (kernel launch)
   int64_t cg_max = 0, cg_min = 0;
   int chunks_per_cta = 4;
-  int direct_mode = 2;     // LANE_DIRECT: registered multi-GPU job set (2 push, 3 pull-all, 0 staged)
+  int direct_mode = 2;     // LANE_DIRECT: registered multi-GPU job set (2 push, 3 pull-all, 4 pull-push, 0 staged)
   int direct_emu = 1;      // LANE_DIRECT in emulated mode (1 direct-pull default)
   bool emu_handshake = false;  // LANE_EMU_HANDSHAKE=1 (tests): start/end handshake in emulated mode
   int sig_skew = -1;       // LANE_EMU_SIG_SKEW_RANK (tests): that emulated rank publishes a wrong signature
@@ -357,9 +357,9 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     c->phase2_ring = p2 && strcmp(p2, "ring") == 0;
   }
   c->direct_mode = (int)env_i64("LANE_DIRECT", 2);
-  if (c->direct_mode != 0 && c->direct_mode != 3) c->direct_mode = 2;  // 1 (pull) exists only emulated
+  if (c->direct_mode != 0 && c->direct_mode != 3 && c->direct_mode != 4) c->direct_mode = 2;  // 1 (pull): emulated only
   c->direct_emu = (int)env_i64("LANE_DIRECT", 1);
-  if (c->direct_emu < 0 || c->direct_emu > 3) c->direct_emu = 1;
+  if (c->direct_emu < 0 || c->direct_emu > 4) c->direct_emu = 1;
   c->emu_handshake = env_i64("LANE_EMU_HANDSHAKE", 0) != 0;
   c->sig_skew = emulated ? (int)env_i64("LANE_EMU_SIG_SKEW_RANK", -1) : -1;
   c->ctas_total = (int)env_i64("LANE_CTAS_TOTAL", 0);

@@ -171,7 +171,12 @@ struct Ctx {
 //    node's sendbufs into my S2 (slot b = sub-part b), C sums the lane
 //    members' S2 slot a into my recvbuf, D pulls the lane members' results
 //    from their recvbufs, E pulls the node peers' parts from theirs.
-enum DirectMode { kStaged = 0, kDirectPull = 1, kDirectPush = 2, kPullAll = 3 };
+//  pull-push (registered user buffers; LANE_DIRECT=4): phase 1 as a pull, the
+//    rest as direct-push: B reads the node peers' sendbufs straight over
+//    NVLink (the start handshake already guarantees they are final), so there
+//    is no A job, no S1 staging and no F1 hop on the chunk's critical path;
+//    C and D push as in direct-push.
+enum DirectMode { kStaged = 0, kDirectPull = 1, kDirectPush = 2, kPullAll = 3, kPullPush = 4 };
 
 __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
   const int dm = x.p->direct;
@@ -185,11 +190,11 @@ __device__ __forceinline__ int njobs(const Ctx& x, int ph) {
     }
   }
   switch (ph) {
-    case 0: return dm == kDirectPull ? 0 : x.G - 1;
+    case 0: return (dm == kDirectPull || dm == kPullPush) ? 0 : x.G - 1;
     case 1: return x.G == 1 ? (dm == kDirectPull ? 0 : x.N - 1) : x.N;
     case 2: return x.N > 1 ? 1 : 0;
     case 3: return dm != kStaged ? ((x.N > 1 && x.G > 1) ? 1 : 0) : x.N - 1;
-    default: return dm == kDirectPush ? 0 : x.G - 1;
+    default: return (dm == kDirectPush || dm == kPullPush) ? 0 : x.G - 1;
   }
 }
 
@@ -203,7 +208,8 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
   const LaneParams& p = *x.p;
   const int a = x.a, g = x.g, N = x.N, G = x.G;
   const bool direct = p.direct == kDirectPull;  // pull flavour (emulated mode)
-  const bool push = p.direct == kDirectPush;
+  const bool push = p.direct == kDirectPush || p.direct == kPullPush;
+  const bool pull1 = direct || p.direct == kPullPush;  // phase 1 reads the node's sendbufs
   J.ph = ph;
   J.nsrc = 1;
   J.ndst = 1;
@@ -287,14 +293,14 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
     J.m0 = ch.g0 + gp.start + up.start;
     J.nsrc = G;
     for (int h = 0; h < G; ++h) {
-      if (direct) {
-        J.src[h] = send_of(p.rk[a * G + h]) + J.m0;
+      if (pull1) {
+        J.src[h] = (h == g ? x.msg.send : send_of(p.rk[a * G + h])) + J.m0;
         J.x_mask |= 1u << h;
       } else {
         J.src[h] = (h == g) ? x.msg.send + J.m0 : s1_slot(p, *x.me, h < g ? h : h - 1, ch.id) + up.start;
       }
     }
-    if (!direct) {
+    if (!pull1) {
       J.x_mask = 1u << g;
       if (t == 0)
         for (int h = 0; h < G; ++h)

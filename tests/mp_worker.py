@@ -49,15 +49,16 @@ def main():
     t0 = time.time()
     maxb = max(counts) * 4
     cases = [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
-             for pr in ("simple", "pull", "ll", "ll128", "ring2", "ring2_128")]
+             for pr in ("simple", "pull", "pullpush", "ll", "ll128", "ring2", "ring2_128")]
     if args.quick:  # the standard multi-PPG approach at PPG 16 (Alg. 1 per slice, P L431), both protocols
         cases += [(1, P, 16, "ll"), (1, P, 16, "ll128")]
     for N, G, k, proto in cases:
         if True:
             # ll / ll128: every call that fits that protocol's inboxes
-            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "ll128": "ll128",
+            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "pullpush": "simple", "ll128": "ll128",
                                         "ring2_128": "ll128"}.get(proto, "ll")
-            os.environ["LANE_DIRECT"] = "3" if proto == "pull" else "2"  # registered job set: push / pull-all
+            # registered job set: push / pull-all / pull-push
+            os.environ["LANE_DIRECT"] = {"pull": "3", "pullpush": "4"}.get(proto, "2")
             if proto.startswith("ring2"):  # the lane method with Alg. 1 as its inter-node stage
                 os.environ["LANE_PHASE2"] = "ring"
             else:

@@ -86,6 +86,7 @@ def set_mode(mode, monkeypatch):
     """Simple-protocol job sets by LANE_DIRECT digit — 1 = direct-pull
     (emulated default), 2 = direct-push (the registered multi-GPU job set),
     3 = pull-all (registered, every job writes only its own rank's memory),
+    4 = pull-push (registered: phase 1 reads the node's sendbufs, C and D push),
     0 = staged (the unregistered job set) — with suffix 'b' = TMA bulk stores
     (LANE_STORE=bulk: what every multi-GPU call >= LANE_BULK_MIN_BYTES runs)
     and 'h' = the start/end handshake with the call signature that every
@@ -104,7 +105,7 @@ def set_mode(mode, monkeypatch):
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "0hb", "2hb", "3hb", "2h", "1b"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "0hb", "2hb", "3hb", "4hb", "2h", "1b"])
 def test_parity_layouts(N, G, dtype, mode, monkeypatch):
     """Every job set / store mode / protocol (set_mode) on every layout, k and
     ragged count, bit-exact vs the oracle."""
@@ -127,7 +128,7 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "0", "ll", "ll128", "mixed", "0hb", "2hb", "3hb"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "mixed", "0hb", "2hb", "3hb", "4hb"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
     """Repeated calls of varying sizes reuse scratch, flags (fixed flag stride:
     one index, one meaning across calls), the handshake's control words and
@@ -456,7 +457,7 @@ def test_ring_parity_ppg_8_16(proto, k, monkeypatch):
                 assert np.array_equal(bits(o), bits(ref)), f"ring P=8 k={k} {dtype} n={n} rank {p}"
 
 
-@pytest.mark.parametrize("mode", ["1", "0hb", "2hb", "3hb", "2h"])
+@pytest.mark.parametrize("mode", ["1", "0hb", "2hb", "3hb", "4hb", "2h"])
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
 def test_whole_buffer_16mib_job_sets(mode, dtype, monkeypatch):
     """Every simple-protocol job set at 16 MiB per rank + a ragged tail (the
