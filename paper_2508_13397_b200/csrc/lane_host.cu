@@ -100,6 +100,7 @@ struct lane_comm_s {
   int chunks_per_cta = 4;
   int direct_mode = 2;     // LANE_DIRECT: registered multi-GPU job set (2 push, 3 pull-all, 4 pull-push, 0 staged)
   int direct_emu = 1;      // LANE_DIRECT in emulated mode (1 direct-pull default)
+  int pdl = 1;             // LANE_PDL: multi-GPU launches with programmatic stream serialization
   bool emu_handshake = false;  // LANE_EMU_HANDSHAKE=1 (tests): start/end handshake in emulated mode
   int sig_skew = -1;       // LANE_EMU_SIG_SKEW_RANK (tests): that emulated rank publishes a wrong signature
   int ctas_total = 0;      // LANE_CTAS_TOTAL: simple-protocol CTAs per GPU (multi-GPU)
@@ -356,6 +357,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     const char* p2 = getenv("LANE_PHASE2");
     c->phase2_ring = p2 && strcmp(p2, "ring") == 0;
   }
+  c->pdl = env_i64("LANE_PDL", 1) != 0;
   c->direct_mode = (int)env_i64("LANE_DIRECT", 2);
   if (c->direct_mode != 0 && c->direct_mode != 3 && c->direct_mode != 4) c->direct_mode = 2;  // 1 (pull): emulated only
   c->direct_emu = (int)env_i64("LANE_DIRECT", 1);
@@ -719,6 +721,29 @@ bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
   return true;
 }
 
+// One kernel launch of a call. Emulated: cooperative (every CTA of every
+// rank co-resident). Multi-GPU: with programmatic stream serialization
+// (LANE_PDL, default on) so the grid is scheduled while the previous grid in
+// the stream drains; every kernel starts with pdl_enter() (lane_kernels.cuh),
+// which waits for that grid's completion before its first memory access.
+cudaError_t launch_kernel(lane_comm_t c, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
+                          cudaStream_t s) {
+  if (c->emulated) return cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s);
+  if (!c->pdl) return cudaLaunchKernel(fn, grid, block, args, smem, s);
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
 // Launch the rounds of a ring_plan (kRingLL, kLaneRingLL, kRingLL128,
 // kLaneRingLL128) or of an a2_plan (kA2LL).
 int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaStream_t s) {
@@ -766,8 +791,7 @@ int ll_ring_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cuda
            : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1, true>
                                    : (const void*)lane::ll::lane_ll_kernel<2, true>;
     const dim3 grid((unsigned)(ranks_here * c->k * pl.C));
-    cudaError_t e = c->emulated ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
-                                : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
+    cudaError_t e = launch_kernel(c, fn, grid, dim3(lane::ll::kThreads), args, 0, s);
     if (e != cudaSuccess)
       return cuda_fail(c, e, lane128   ? "lane_ll128_kernel launch (ring inter-node stage)"
                              : ring128 ? "lane_ring_ll128_kernel launch"
@@ -803,9 +827,7 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
                           : (dtype == LANE_INT32     ? (const void*)lane::ll128::lane_ll128_kernel<0>
                              : dtype == LANE_FLOAT32 ? (const void*)lane::ll128::lane_ll128_kernel<1>
                                                      : (const void*)lane::ll128::lane_ll128_kernel<2>);
-      cudaError_t e = c->emulated
-                          ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s)
-                          : cudaLaunchKernel(fn, grid, dim3(lane::ll128::kThreads), args, 0, s);
+      cudaError_t e = launch_kernel(c, fn, grid, dim3(lane::ll128::kThreads), args, 0, s);
       if (e != cudaSuccess) return cuda_fail(c, e, "lane_ll128_kernel launch");
       continue;
     }
@@ -820,9 +842,7 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
       const void* fn = dtype == LANE_INT32     ? (const void*)lane::ll::lane_ll_kernel<0>
                        : dtype == LANE_FLOAT32 ? (const void*)lane::ll::lane_ll_kernel<1>
                                                : (const void*)lane::ll::lane_ll_kernel<2>;
-      cudaError_t e = c->emulated
-                          ? cudaLaunchCooperativeKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s)
-                          : cudaLaunchKernel(fn, grid, dim3(lane::ll::kThreads), args, 0, s);
+      cudaError_t e = launch_kernel(c, fn, grid, dim3(lane::ll::kThreads), args, 0, s);
       if (e != cudaSuccess) return cuda_fail(c, e, "lane_ll_kernel launch");
       continue;
     }
@@ -845,10 +865,7 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
       fn = dtype == LANE_INT32     ? (const void*)lane::lane_allreduce_kernel<0>
            : dtype == LANE_FLOAT32 ? (const void*)lane::lane_allreduce_kernel<1>
                                    : (const void*)lane::lane_allreduce_kernel<2>;
-    if (c->emulated)
-      e = cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s);
-    else
-      e = cudaLaunchKernel(fn, grid, block, args, smem, s);
+    e = launch_kernel(c, fn, grid, block, args, smem, s);
     if (e != cudaSuccess) return cuda_fail(c, e, "lane_allreduce_kernel launch");
   }
   return LANE_OK;

@@ -54,6 +54,29 @@ __device__ __forceinline__ void st_relaxed_sys(uint32_t* p, uint32_t v) {
   asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
+// Programmatic dependent launch (PDL). The host launches every multi-GPU call
+// with cudaLaunchAttributeProgrammaticStreamSerialization, so the next grid
+// in the stream may be scheduled before this one has finished. Each kernel
+// first waits until the previous grid in the stream has completed and its
+// memory operations are visible (griddepcontrol.wait; a no-op for a launch
+// without a programmatic dependency), so stream order is kept for every
+// access, then allows the next grid to launch (launch_dependents): the next
+// call's CTAs are dispatched onto SMs as this call's CTAs exit and wait there,
+// instead of paying the launch latency after the last CTA is gone.
+__device__ __forceinline__ void pdl_enter() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// Every kernel of a comm starts here (PDL wait; pdl_enter).
+__device__ __forceinline__ void launch_prologue(const LaneParams&) { pdl_enter(); }
+
+__device__ __forceinline__ uint32_t smid() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r));
+  return r;
+}
+
 __device__ __forceinline__ uint64_t globaltimer_ns() {
   uint64_t t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -245,6 +268,7 @@ constexpr int kFanBatch = 4;   // sources loaded together in reduce phases
 
 template <int DT>
 __global__ void __launch_bounds__(512, 1) lane_allreduce_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int rank = p.rank0 + (int)(blockIdx.x / per_rank);

@@ -213,12 +213,14 @@ __device__ __forceinline__ void phase_clock_flush(const LaneParams& p, const Pha
   if (p.trace == nullptr) return;
   __syncthreads();
   if (threadIdx.x < 8) p.trace[(size_t)blockIdx.x * kTraceWords + threadIdx.x] = pc.t[threadIdx.x];
+  if (threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceWords + kTrSmid] = smid();
 }
 
 // RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a
 // separate instantiation so the default kernel keeps its register budget.
 template <int DT, bool RING2 = false>
 __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   __shared__ uint64_t clk[8];
   const PhaseClock pc = phase_clock_begin(p, clk);
   using O = Ops<DT>;
@@ -429,6 +431,7 @@ LANE_HD int64_t ring_set_granules(int P, int64_t ring_slot) { return 2 * (int64_
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ring_ll_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int r = p.rank0 + (int)(blockIdx.x / per_rank);
@@ -515,6 +518,7 @@ LANE_HD int64_t a2_set_granules(int G, int N, int64_t slot_g, int64_t slot_v) {
 
 template <int DT>
 __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_a2_ll_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int rank = p.rank0 + (int)(blockIdx.x / per_rank);

@@ -48,6 +48,7 @@ constexpr int kLineGranules = 7;  // data granules per 128-byte line
 constexpr int kLineBytes = 128;
 constexpr unsigned kFull = 0xffffffffu;
 
+
 // Lines of a sub-part slot for a chunk whose sub-parts hold at most su granules.
 LANE_HD int64_t lines_of(int64_t su) { return ceil_div(su, kLineGranules); }
 
@@ -131,14 +132,19 @@ struct BatchT {
   int32_t ln[U], i[U];  // line in the sub-part, chunk-relative granule (< 2^31: 32-bit, fewer registers)
 };
 
-// Warp-collective: fetch U lines (inactive lines read as zero, never loaded)
-// and wait until every active line carries the epoch.
+// Issue the loads of U lines (inactive lines read as zero, never loaded).
 template <int U>
-__device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U], int sl,
-                                          uint4 (&v)[U]) {
-  bool got[U], all = true;
+__device__ __forceinline__ void fetch_lines(const uint4* const (&ptr)[U], const bool (&act)[U], int sl, uint4 (&v)[U]) {
 #pragma unroll
   for (int u = 0; u < U; ++u) v[u] = act[u] ? line_load(ptr[u], sl) : make_uint4(0, 0, 0, 0);
+}
+
+// Warp-collective: wait until every active fetched line carries the epoch
+// (reloading the ones that did not yet).
+template <int U>
+__device__ __forceinline__ bool check_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U],
+                                            int sl, uint4 (&v)[U]) {
+  bool got[U], all = true;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
     const bool r = group_ready(v[u], sl, p.epoch);
@@ -154,6 +160,14 @@ __device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* cons
       v[u] = w.v;
     }
   return true;
+}
+
+// Warp-collective: fetch U lines and wait until every active line carries the epoch.
+template <int U>
+__device__ __forceinline__ bool get_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U], int sl,
+                                          uint4 (&v)[U]) {
+  fetch_lines(ptr, act, sl, v);
+  return check_lines(p, ptr, act, sl, v);
 }
 
 // Line index within a parity set of the lane kernel's inboxes for a call
@@ -249,6 +263,7 @@ inline int64_t set_capacity128(int G, int N, int k, int64_t M, int64_t cg_min) {
 // instantiation so the default kernel keeps its register budget.
 template <int DT, bool RING2 = false, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   using Batch = BatchT<U>;
   __shared__ uint64_t clk[8];
   const ll::PhaseClock pc = ll::phase_clock_begin(p, clk);
@@ -315,24 +330,67 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
     return true;
   };
 
-  // ---------------- A: phase-1 push of the node peers' parts (t = 1..G-1 -> peer gd = g+t)
-  for (int64_t c = j; c < nc; c += p.C) {
-    const ChunkGeo ch = geo(c);
-    auto span = [&](int t, int b) {
-      const Span pd = rf_split(ch.len, G, (g + 1 + t) % G);
-      Span up = rf_split(pd.len, N, b);
+  // The default path (not RING2) runs every phase through `phase`: warp step
+  // s of chunk ch covers positions 4*U*s .. 4*U*s + 4*U - 1 of the chunk's
+  // flat space; CTA j takes its chunks j, j+C, ..., warp w the steps w,
+  // w + 16, ... (a static share). A pooled variant — the last half of every
+  // chunk's steps claimed by any warp of the rank through per-phase atomic
+  // counters, so fast SMs take the slow ones' tail (per-SM push rates differ
+  // up to 2x, profiles/r02_trace_smid_p4.txt) — balanced the phase ends but
+  // was slower at every size: the phases are link-bound, not
+  // imbalance-bound.
+  auto step = [&](const ChunkGeo& ch, int64_t s, int T, int NB, auto span, auto f) -> bool {
+    const int64_t total = (int64_t)T * NB * lu;
+    const int64_t V0 = s * 4 * U;
+    Batch q;
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = V0 + 4 * u + grp;
+      q.act[u] = v < total;
+      const uint32_t v32 = q.act[u] ? (uint32_t)v : 0u, lu32 = (uint32_t)lu;
+      const uint32_t r = v32 / lu32;
+      q.ln[u] = (int32_t)(v32 - r * lu32);
+      q.b[u] = (int)(r % (uint32_t)NB);
+      q.t[u] = (int)(r / (uint32_t)NB);
+      const Span up = span(ch, q.t[u], q.b[u]);
+      q.act[u] = q.act[u] && q.ln[u] < lines_of(up.len);
+      q.i[u] = q.ln[u] * kLineGranules + sl;
+      q.dv[u] = q.act[u] && sl < kLineGranules && q.i[u] < up.len;
+      q.i[u] += (int32_t)up.start;
+    }
+    return f(ch, q);
+  };
+  auto phase = [&](int T, int NB, auto span, auto f) -> bool {
+    const int64_t ns = ceil_div((int64_t)T * NB * lu, 4 * U);  // warp steps per chunk
+    for (int64_t c = j; c < nc; c += p.C) {
+      const ChunkGeo ch = geo(c);
+      for (int64_t s = warp; s < ns; s += kWarps)
+        if (!step(ch, s, T, NB, span, f)) return false;
+    }
+    return true;
+  };
+
+  // ---------------- A: phase-1 push of the node peers' parts. Flat order
+  // (t, b, ln): t = sub-part order (sub-part (a+1+t) % N, the order phase B
+  // consumes them in), b = destination (node peer gd = g+1+b), so the lines
+  // every receiver needs first are pushed first by all its node peers.
+  {
+    auto span = [&](const ChunkGeo& ch, int t, int b) {
+      const Span pd = rf_split(ch.len, G, (g + 1 + b) % G);
+      Span up = rf_split(pd.len, N, (a + 1 + t) % N);
       up.start += pd.start;  // granule offset within the chunk
       return up;
     };
-    walk(G - 1, N, span, [&](const Batch& q) {
+    phase(N, G - 1, span, [&](const ChunkGeo& ch, const Batch& q) {
       uint4 x[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) x[u] = q.dv[u] ? load_x(msg, ch.g0 + q.i[u]) : z;
 #pragma unroll
       for (int u = 0; u < U; ++u)
         if (q.act[u]) {
-          const int gd = (g + 1 + q.t[u]) % G;
-          line_store(inbox_of(p, p.rk[a * G + gd]).l1(slot_of(g, gd), ch.id, q.b[u], q.ln[u]), sl, x[u], ep);
+          const int gd = (g + 1 + q.b[u]) % G;
+          line_store(inbox_of(p, p.rk[a * G + gd]).l1(slot_of(g, gd), ch.id, (a + 1 + q.t[u]) % N, q.ln[u]), sl,
+                     x[u], ep);
         }
       return true;
     });
@@ -453,33 +511,47 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
 
   // ---------------- B: phase-1 reduce (ascending h) -> phase-2 reduce-scatter push
   // (t = 0..N-1 -> sub-part b = a+1+t: remote sub-parts first, own last)
-  for (int64_t c = j; c < nc; c += p.C) {
-    const ChunkGeo ch = geo(c);
-    const Span gp = rf_split(ch.len, G, g);
-    auto span = [&](int t, int) {
+  {
+    auto span = [&](const ChunkGeo& ch, int t, int) {
+      const Span gp = rf_split(ch.len, G, g);
       Span up = rf_split(gp.len, N, (a + 1 + t) % N);
       up.start += gp.start;
       return up;
     };
-    const bool ok = walk(N, 1, span, [&](const Batch& q) {
+    const bool ok = phase(N, 1, span, [&](const ChunkGeo& ch, const Batch& q) {
       typename O::Acc acc[U];
-      for (int h = 0; h < G; ++h) {  // warp-uniform, ascending (R#7)
-        uint4 v[U];
+      // the node's G terms two at a time: both terms' loads (own sendbuf or a
+      // peer's lines) are in flight before the first epoch check — one round
+      // trip per pair instead of one per term; summed ascending (R#7)
+      auto fetch_term = [&](int h, const uint4* (&ptr)[U], uint4 (&v)[U]) {
         if (h == g) {
 #pragma unroll
           for (int u = 0; u < U; ++u) v[u] = q.dv[u] ? load_x(msg, ch.g0 + q.i[u]) : z;
         } else {
-          const uint4* ptr[U];
 #pragma unroll
           for (int u = 0; u < U; ++u) ptr[u] = me.l1(slot_of(h, g), ch.id, (a + 1 + q.t[u]) % N, q.ln[u]);
-          if (!get_lines(p, ptr, q.act, sl, v)) return false;
+          fetch_lines(ptr, q.act, sl, v);
         }
+      };
+      for (int h0 = 0; h0 < G; h0 += 2) {  // warp-uniform
+        const int h1 = h0 + 1;
+        const uint4* p0[U];
+        const uint4* p1[U];
+        uint4 v0[U], v1[U];
+        fetch_term(h0, p0, v0);
+        if (h1 < G) fetch_term(h1, p1, v1);
+        if (h0 != g && !check_lines(p, p0, q.act, sl, v0)) return false;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (h == 0)
-            O::init(acc[u], v[u]);
+          if (h0 == 0)
+            O::init(acc[u], v0[u]);
           else
-            O::add(acc[u], v[u]);
+            O::add(acc[u], v0[u]);
+        }
+        if (h1 < G) {
+          if (h1 != g && !check_lines(p, p1, q.act, sl, v1)) return false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) O::add(acc[u], v1[u]);
         }
       }
 #pragma unroll
@@ -495,28 +567,40 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
   pc.end(2);
 
   // ---------------- C: phase-2 reduce (ascending b) -> recvbuf + lane AG + phase-3 forward
-  for (int64_t c = j; c < nc; c += p.C) {
-    const ChunkGeo ch = geo(c);
-    const Span gp = rf_split(ch.len, G, g);
-    auto span = [&](int, int) {
+  {
+    auto span = [&](const ChunkGeo& ch, int, int) {
+      const Span gp = rf_split(ch.len, G, g);
       Span up = rf_split(gp.len, N, a);
       up.start += gp.start;
       return up;
     };
-    const bool ok = walk(1, 1, span, [&](const Batch& q) {
+    const bool ok = phase(1, 1, span, [&](const ChunkGeo& ch, const Batch& q) {
       typename O::Acc acc[U];
-      for (int b = 0; b < N; ++b) {  // warp-uniform, ascending (R#7)
-        uint4 v[U];
-        const uint4* ptr[U];
+      for (int b0 = 0; b0 < N; b0 += 2) {  // warp-uniform; two lane terms in flight, ascending (R#7)
+        const int b1 = b0 + 1;
+        uint4 v0[U], v1[U];
+        const uint4* p0[U];
+        const uint4* p1[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) ptr[u] = me.l2(b, ch.id, q.ln[u]);
-        if (!get_lines(p, ptr, q.act, sl, v)) return false;
+        for (int u = 0; u < U; ++u) p0[u] = me.l2(b0, ch.id, q.ln[u]);
+        fetch_lines(p0, q.act, sl, v0);
+        if (b1 < N) {
+#pragma unroll
+          for (int u = 0; u < U; ++u) p1[u] = me.l2(b1, ch.id, q.ln[u]);
+          fetch_lines(p1, q.act, sl, v1);
+        }
+        if (!check_lines(p, p0, q.act, sl, v0)) return false;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (b == 0)
-            O::init(acc[u], v[u]);
+          if (b0 == 0)
+            O::init(acc[u], v0[u]);
           else
-            O::add(acc[u], v[u]);
+            O::add(acc[u], v0[u]);
+        }
+        if (b1 < N) {
+          if (!check_lines(p, p1, q.act, sl, v1)) return false;
+#pragma unroll
+          for (int u = 0; u < U; ++u) O::add(acc[u], v1[u]);
         }
       }
 #pragma unroll
@@ -542,16 +626,14 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
 
   // ---------------- D: phase-2 allgather receive -> recvbuf + phase-3 forward
   // (t = 0..N-2 -> lane peer b = a+1+t)
-  if (N > 1)
-    for (int64_t c = j; c < nc; c += p.C) {
-      const ChunkGeo ch = geo(c);
-      const Span gp = rf_split(ch.len, G, g);
-      auto span = [&](int t, int) {
+  if (N > 1) {
+      auto span = [&](const ChunkGeo& ch, int t, int) {
+        const Span gp = rf_split(ch.len, G, g);
         Span up = rf_split(gp.len, N, (a + 1 + t) % N);
         up.start += gp.start;
         return up;
       };
-      const bool ok = walk(N - 1, 1, span, [&](const Batch& q) {
+      const bool ok = phase(N - 1, 1, span, [&](const ChunkGeo& ch, const Batch& q) {
         uint4 v[U];
         const uint4* ptr[U];
 #pragma unroll
@@ -576,15 +658,14 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
   }  // !RING2
 
   // ---------------- E: phase-3 allgather receive (t = 0..G-2 -> node peer h = g+1+t)
-  for (int64_t c = j; c < nc; c += p.C) {
-    const ChunkGeo ch = geo(c);
-    auto span = [&](int t, int b) {
+  {
+    auto span = [&](const ChunkGeo& ch, int t, int b) {
       const Span ph = rf_split(ch.len, G, (g + 1 + t) % G);
       Span up = rf_split(ph.len, N, b);
       up.start += ph.start;
       return up;
     };
-    const bool ok = walk(G - 1, N, span, [&](const Batch& q) {
+    const bool ok = phase(G - 1, N, span, [&](const ChunkGeo& ch, const Batch& q) {
       uint4 v[U];
       const uint4* ptr[U];
 #pragma unroll
@@ -637,6 +718,7 @@ LANE_HD RingLayout128 ring_layout128(int P, int64_t cap, int64_t lp) {
 
 template <int DT, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __grid_constant__ LaneParams p) {
+  launch_prologue(p);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int r = p.rank0 + (int)(blockIdx.x / per_rank);

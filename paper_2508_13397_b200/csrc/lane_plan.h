@@ -110,6 +110,7 @@ enum TraceField {
   kTrStartAbs,   // producer start (absolute globaltimer)
   kTrEnterWait,  // producer time in the start-of-call handshake
   kTrEndAbs,     // releaser past the end-of-call barrier (absolute; rank's last CTA only)
+  kTrSmid,       // SM the CTA ran on (%smid)
   kTraceWords
 };
 

@@ -5,6 +5,7 @@ python tools/trace_run.py --emulated --layout 2x4
 Prints, per rank, the mean / max over CTAs of every trace field in microseconds.
 """
 import argparse
+import json
 import os
 import statistics
 import sys
@@ -31,6 +32,34 @@ def summarize_ll(tr, label):
         if v:
             out.append(f"  end of phase {ph}   min {(min(v) - t0) / 1e3:9.2f}  max {(max(v) - t0) / 1e3:9.2f}")
     return "\n".join(out)
+
+
+def smid_report(tr, label, key):
+    """Does a CTA's time to finish `key` follow the SM it ran on? Mean per SM
+    class (smid halves, parity, TPC pairs) and the SMs of the 12 slowest and
+    fastest CTAs."""
+    rows = [(t["smid"], t[key]) for t in tr if t.get(key)]
+    if not rows:
+        return ""
+    vals = sorted(rows, key=lambda r: r[1])
+    m = statistics.mean(v for _, v in rows)
+
+    def cls(name, f):
+        a = [v for s, v in rows if f(s)]
+        b = [v for s, v in rows if not f(s)]
+        return f"{name}: {statistics.mean(a) / m:.3f} vs {statistics.mean(b) / m:.3f}" if a and b else ""
+    out = [f"  {label} {key}: per-SM classes (mean / overall mean): " +
+           "; ".join(x for x in (cls("smid<74", lambda s: s < 74), cls("even smid", lambda s: s % 2 == 0),
+                                 cls("smid%4<2", lambda s: s % 4 < 2), cls("smid%16<8", lambda s: s % 16 < 8)) if x)]
+    out.append("  slowest SMs: " + " ".join(str(s) for s, _ in vals[-12:][::-1]))
+    out.append("  fastest SMs: " + " ".join(str(s) for s, _ in vals[:12]))
+    return "\n".join(out)
+
+
+def dump(tr, ll, path):
+    with open(path, "a") as f:
+        for i, t in enumerate(tr):
+            f.write(json.dumps(dict(t, cta=i, ll=ll)) + "\n")
 
 
 def summarize(tr, label):
@@ -60,6 +89,7 @@ def main():
     ap.add_argument("--dtype", default="float32")
     ap.add_argument("--emulated", action="store_true")
     ap.add_argument("--register", action="store_true", help="register the buffers (direct-push job set, as bench.py)")
+    ap.add_argument("--dump", default=None, help="append every CTA's trace record (JSON lines) to this file")
     ap.add_argument("--calls", type=int, default=1,
                     help="back-to-back calls before reading the trace (>1: steady state, no launch skew)")
     a = ap.parse_args()
@@ -98,7 +128,15 @@ def main():
     torch.cuda.synchronize()
     tr = comm.trace()
     summ = summarize_ll if comm.protocol(n, a.dtype) in ("ll", "ll128") else summarize
+    ll = comm.protocol(n, a.dtype) in ("ll", "ll128")
     txt = summ(tr, f"rank {rank} {a.layout} k={a.k} ctas={len(tr)} kernel {s.elapsed_time(e) / a.calls:.4f} ms/call over {a.calls} calls")
+    if ll:  # phase-A end (word 1) relative to the CTA's start (word 0)
+        tr2 = [dict(t, a_time=t[lane.LaneComm.TRACE_FIELDS[1]] - t[lane.LaneComm.TRACE_FIELDS[0]]) for t in tr]
+        txt += "\n" + smid_report(tr2, f"rank {rank}", "a_time")
+    else:
+        txt += "\n" + smid_report(tr, f"rank {rank}", "phase_A")
+    if a.dump:
+        dump(tr, ll, a.dump.replace("%r", str(rank)))
     for r in range(dist.get_world_size()):
         if r == rank:
             print(txt, flush=True)
