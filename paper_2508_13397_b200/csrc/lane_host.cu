@@ -339,8 +339,13 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   // LL128 ahead of LL above 1 MiB (2 MiB at P = 2), ahead of simple up to 16 MiB
   c->ll128_max = env_i64("LANE_LL128_MAX_BYTES", 32 << 20) / 16;
   if (c->ll128_max < 0) c->ll128_max = 0;
-  c->ll128_lo = env_i64("LANE_LL128_MIN_BYTES", (N * G == 2 ? 2 : 1) << 20) / 16;
-  c->ll128_hi = env_i64("LANE_LL128_THRESHOLD_BYTES", 16 << 20) / 16;
+  // Default protocol ranges, from the measured crossovers (profiles/r02_protocol_crossovers.txt,
+  // P = 2 and 4, every layout): LL128 beats LL from 1 MiB at P = 4 (above 512 KiB) and from
+  // 4 MiB at P = 2; the simple protocol beats LL128 above 32 MiB when both phases span GPUs
+  // (N > 1, G > 1: four dependent hops per chunk), above 24 MiB for one-GPU nodes (G = 1),
+  // above 16 MiB for one node (N = 1).
+  c->ll128_lo = env_i64("LANE_LL128_MIN_BYTES", N * G == 2 ? (2 << 20) : (512 << 10)) / 16;
+  c->ll128_hi = env_i64("LANE_LL128_THRESHOLD_BYTES", (N > 1 && G > 1) ? (32 << 20) : (G == 1 ? (24 << 20) : (16 << 20))) / 16;
   c->ll128_cg_min = env_i64("LANE_LL128_MIN_CHUNK_BYTES", 16 << 10) / 16;
   c->ll128_u1_max = env_i64("LANE_LL128_U1_MAX_BYTES", 4 << 20) / 16;
   if (c->ll128_cg_min < 64) c->ll128_cg_min = 64;

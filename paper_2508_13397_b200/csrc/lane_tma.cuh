@@ -136,6 +136,7 @@ struct Job {
   uint32_t x_mask;       // bit i: src[i] is a sendbuf (partial last granule possible)
   uint32_t recv_mask;    // bit d: dst[d] is a recvbuf
   int nwait, nrel;
+  int entry;    // needs the start handshake first: writes a recvbuf or reads a peer's sendbuf
   int64_t len;  // granules
   int64_t m0;   // message granule of the job's first granule
   const uint4* src[kMaxSrc];
@@ -204,7 +205,7 @@ __device__ __forceinline__ uint4* send_of(const RankMem& m) {
 __device__ __forceinline__ uint4* recv_of(const RankMem& m) { return reinterpret_cast<uint4*>(m.recv); }
 
 // Job t of phase ph (0=A .. 4=E) for chunk ch.
-__device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
+__device__ void make_job_(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
   const LaneParams& p = *x.p;
   const int a = x.a, g = x.g, N = x.N, G = x.G;
   const bool direct = p.direct == kDirectPull;  // pull flavour (emulated mode)
@@ -411,6 +412,21 @@ __device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J
     J.dst[0] = x.msg.recv + J.m0;
     J.recv_mask = 1;
   }
+}
+
+// make_job_ plus J.entry. Jobs that only move data into peers' SCRATCH (S1,
+// S2) may run before the start handshake: a peer reads its scratch of call e
+// before it passes the end barrier of call e, which this rank passed before
+// starting call e+1, and every scratch read is gated by its epoch flag. Jobs
+// that write any recvbuf or read a peer's sendbuf wait for the handshake (the
+// peer's kernel has started, so its stream's earlier work on those buffers is
+// done, and its call signature matches ours).
+__device__ void make_job(const Ctx& x, int ph, const ChunkGeo& ch, int t, Job& J) {
+  make_job_(x, ph, ch, t, J);
+  int e = J.recv_mask != 0;
+  for (int i = 0; i < J.nsrc && !e; ++i)
+    if ((J.x_mask >> i) & 1u) e = J.src[i] < x.msg.send || J.src[i] >= x.msg.send + x.p->ng;  // a peer's sendbuf
+  J.entry = e;
 }
 
 __device__ __forceinline__ int64_t tile_granules(int nsrc) {
@@ -677,27 +693,41 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     const int64_t window = 6;
     int64_t k = 0;  // global tile counter
     bool ok = true;
-    if (p.handshake) {
-      // start of call: a peer's sendbuf is final and its recvbuf free once its
-      // kernel has started (stream order). The first CTA of each rank also
-      // publishes the call signature (host call_signature: job set, buffer
-      // offsets in the registrations, count, dtype, chunking) before its enter
-      // flag; every CTA compares every peer's with its own, so ranks that
-      // disagree (one zero-copy, one staged; different offsets or counts)
-      // stop here with LANE_ERR_MISMATCH before touching any buffer, instead
-      // of exchanging wrong data or waiting for flags that never come. The
-      // sig slots are rewritten only in the next call, after the end barrier.
-      const uint32_t my_sig = p.sig ^ (x.rank == p.sig_skew ? 1u : 0u);
-      if (blockIdx.x % per_rank == 0) {
-        for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlSig + x.rank, my_sig);
-        fence_acq_rel_sys();
-        for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlEnter + x.rank, p.epoch);
+    // Start-of-call handshake (every simple-protocol call on real peers): a
+    // peer's sendbuf is final and its recvbuf free once its kernel has started
+    // (stream order). The first CTA of each rank publishes the call signature
+    // (host call_signature: job set, buffer offsets in the registrations,
+    // count, dtype, chunking) and then its enter flag; every CTA compares
+    // every peer's signature with its own before its first job that writes a
+    // recvbuf or reads a peer's sendbuf (Job::entry), so ranks that disagree
+    // (one zero-copy, one staged; other offsets or counts) stop with
+    // LANE_ERR_MISMATCH before touching a user buffer, instead of exchanging
+    // wrong data or waiting for flags that never come. Scratch-only jobs (A,
+    // B into S1/S2) run meanwhile, so the handshake's round trip overlaps
+    // data movement. The sig slots are rewritten only in the next call,
+    // after the end barrier.
+    const uint32_t my_sig = p.sig ^ (x.rank == p.sig_skew ? 1u : 0u);
+    bool entered = !p.handshake;
+    int enter_seen = 0;  // peers (in rank order, skipping this one) whose enter flag was seen
+    if (p.handshake && blockIdx.x % per_rank == 0) {
+      for (int q = 0; q < p.P; ++q)
+        if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlSig + x.rank, my_sig);
+      fence_acq_rel_sys();
+      for (int q = 0; q < p.P; ++q)
+        if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlEnter + x.rank, p.epoch);
+    }
+    // Non-blocking: true once every peer's enter flag is set and the
+    // signatures agree (ok = false on a mismatch).
+    auto try_enter = [&]() -> bool {
+      while (enter_seen < p.P) {
+        if (enter_seen == x.rank) {
+          ++enter_seen;
+          continue;
+        }
+        if (!flag_ready(p, x.me->flags + p.ctl + kCtlEnter + enter_seen)) return false;
+        ++enter_seen;
       }
-      for (int q = 0; q < p.P && ok; ++q)
-        if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + kCtlEnter + q)) ok = false;
-      for (int q = 0; q < p.P && ok; ++q) {
+      for (int q = 0; q < p.P; ++q) {
         if (q == x.rank) continue;
         uint32_t v;
         asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(x.me->flags + p.ctl + kCtlSig + q) : "memory");
@@ -706,11 +736,14 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
           *reinterpret_cast<volatile uint32_t*>(p.err) = (uint32_t)(-LANE_ERR_MISMATCH);
           __threadfence_system();
           ok = false;
+          return false;
         }
       }
-      if (ok) fence_async_global();
+      fence_async_global();
       if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEnterWait] = globaltimer_ns() - t_start;
-    }
+      entered = true;
+      return true;
+    };
     if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrStartAbs] = t_start;
     uint64_t t_idle = 0;
     while (ok) {
@@ -727,6 +760,10 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
           wpos[ph] = 0;
         }
         const Job& Jc = jobs[ph];
+        if (Jc.entry && !entered && !try_enter()) {
+          if (!ok) break;
+          continue;
+        }
         while (wpos[ph] < Jc.nwait && flag_ready(p, Jc.wait[wpos[ph]])) ++wpos[ph];
         if (wpos[ph] == Jc.nwait) pick = ph;
       }
