@@ -829,9 +829,21 @@ def staged_multi(comm, inp, N, G, dtype, n, S, args, dist, stream):
 
 def e2e_multi(comm, inp, N, G, dtype, n, S, args, dist):
     import torch
-    h_in = torch.empty(n, dtype=inp.dtype).pin_memory()
-    h_in.copy_(inp)
-    h_out = torch.empty_like(h_in).pin_memory()
+    # 2 x S of pinned host memory per rank (16 GiB at 8 ranks x 1 GiB): every
+    # rank allocates first and the ranks agree before any collective timing,
+    # so one rank short of pinned memory cannot leave the others in a barrier
+    err = None
+    try:
+        h_in = torch.empty(n, dtype=inp.dtype).pin_memory()
+        h_in.copy_(inp)
+        h_out = torch.empty_like(h_in).pin_memory()
+    except (RuntimeError, MemoryError) as e:  # pinned allocation failed
+        err = str(e).splitlines()[0][:200]
+    bad = torch.tensor([0 if err is None else 1])
+    dist.all_reduce(bad)
+    if int(bad.item()):
+        return {"value": None, "unit": "GB/s", "h2d_bytes_per_step": S, "d2h_bytes_per_step": S,
+                "error": err or "pinned host allocation failed on another rank"}
     stream = torch.cuda.current_stream()
     ms = device_time_ms(lambda: comm.allreduce_host(h_out, h_in), args.e2e_steps, 1, stream,
                         lambda: dist.barrier())

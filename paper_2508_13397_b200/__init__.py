@@ -131,7 +131,7 @@ class _CommBase:
     TRACE_FIELDS = ("prod_total", "prod_flag_wait", "prod_empty_wait", "prod_tiles", "store_total",
                     "store_full_wait", "store_sync", "store_read_wait", "store_flush", "store_jobs",
                     "phase_A", "phase_B", "phase_C", "phase_D", "phase_E", "bytes_stored",
-                    "start_abs", "enter_wait", "end_abs", "smid")
+                    "start_abs", "enter_wait", "end_abs", "smid", "entry_abs")
 
     def trace(self) -> list:
         """Per-CTA stall accounting of the last launch (needs LANE_TRACE=1 at

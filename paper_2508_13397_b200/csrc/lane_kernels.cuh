@@ -68,8 +68,15 @@ __device__ __forceinline__ void pdl_enter() {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
-// Every kernel of a comm starts here (PDL wait; pdl_enter).
-__device__ __forceinline__ void launch_prologue(const LaneParams&) { pdl_enter(); }
+__device__ __forceinline__ uint64_t globaltimer_ns();
+
+// Every kernel of a comm starts here (PDL wait; pdl_enter). Returns the time
+// the CTA began, before the wait (trace: how early PDL dispatched it).
+__device__ __forceinline__ uint64_t launch_prologue(const LaneParams&) {
+  const uint64_t t = globaltimer_ns();
+  pdl_enter();
+  return t;
+}
 
 __device__ __forceinline__ uint32_t smid() {
   uint32_t r;

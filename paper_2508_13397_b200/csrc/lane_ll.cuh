@@ -200,10 +200,10 @@ struct PhaseClock {
   }
 };
 
-__device__ __forceinline__ PhaseClock phase_clock_begin(const LaneParams& p, uint64_t* sh) {
+__device__ __forceinline__ PhaseClock phase_clock_begin(const LaneParams& p, uint64_t* sh, uint64_t t_entry) {
   PhaseClock pc{&p, sh};
   if (p.trace != nullptr) {
-    if (threadIdx.x < 8) sh[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : 0;
+    if (threadIdx.x < 8) sh[threadIdx.x] = threadIdx.x == 0 ? globaltimer_ns() : (threadIdx.x == 6 ? t_entry : 0);
     __syncthreads();
   }
   return pc;
@@ -214,15 +214,16 @@ __device__ __forceinline__ void phase_clock_flush(const LaneParams& p, const Pha
   __syncthreads();
   if (threadIdx.x < 8) p.trace[(size_t)blockIdx.x * kTraceWords + threadIdx.x] = pc.t[threadIdx.x];
   if (threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceWords + kTrSmid] = smid();
+  if (threadIdx.x == 0) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEntryAbs] = pc.t[6];
 }
 
 // RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a
 // separate instantiation so the default kernel keeps its register budget.
 template <int DT, bool RING2 = false>
 __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(const __grid_constant__ LaneParams p) {
-  launch_prologue(p);
+  const uint64_t t_entry = launch_prologue(p);
   __shared__ uint64_t clk[8];
-  const PhaseClock pc = phase_clock_begin(p, clk);
+  const PhaseClock pc = phase_clock_begin(p, clk, t_entry);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int rank = p.rank0 + (int)(blockIdx.x / per_rank);

@@ -263,10 +263,10 @@ inline int64_t set_capacity128(int G, int N, int k, int64_t M, int64_t cg_min) {
 // instantiation so the default kernel keeps its register budget.
 template <int DT, bool RING2 = false, int U = LANE_LL128_U>
 __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_constant__ LaneParams p) {
-  launch_prologue(p);
+  const uint64_t t_entry = launch_prologue(p);
   using Batch = BatchT<U>;
   __shared__ uint64_t clk[8];
-  const ll::PhaseClock pc = ll::phase_clock_begin(p, clk);
+  const ll::PhaseClock pc = ll::phase_clock_begin(p, clk, t_entry);
   using O = Ops<DT>;
   const int per_rank = p.k * p.C;
   const int rank = p.rank0 + (int)(blockIdx.x / per_rank);

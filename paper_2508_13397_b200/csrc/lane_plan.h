@@ -111,6 +111,7 @@ enum TraceField {
   kTrEnterWait,  // producer time in the start-of-call handshake
   kTrEndAbs,     // releaser past the end-of-call barrier (absolute; rank's last CTA only)
   kTrSmid,       // SM the CTA ran on (%smid)
+  kTrEntryAbs,   // CTA entry before the PDL wait (absolute)
   kTraceWords
 };
 

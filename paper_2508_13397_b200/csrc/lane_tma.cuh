@@ -546,7 +546,7 @@ __device__ __forceinline__ ChunkGeo chunk_geo(const LaneParams& p, int64_t cb, c
 
 template <int DT, bool kLsuStore>
 __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel(const __grid_constant__ LaneParams p) {
-  launch_prologue(p);
+  const uint64_t t_entry = launch_prologue(p);
   using O = Ops<DT>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + kStages * kStageBytes);
@@ -864,6 +864,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       Tr[kTrProdEmptyWait] = tr_empty;
       Tr[kTrProdTiles] = (uint64_t)k;
       Tr[kTrSmid] = smid();
+      Tr[kTrEntryAbs] = t_entry;
     }
     return;
   }

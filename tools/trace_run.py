@@ -27,6 +27,9 @@ def summarize_ll(tr, label):
     t0 = min(r[0] for r in rows)
     out = [label + f"  (LL protocol, {len(rows)} CTAs; us after the first CTA started)"]
     out.append(f"  CTA start        min {0:9.2f}  max {(max(r[0] for r in rows) - t0) / 1e3:9.2f}")
+    ent = [t["entry_abs"] for t in tr if t.get("entry_abs")]
+    if ent:  # before the PDL wait: how early the CTAs were resident
+        out.append(f"  CTA entry (pre-PDL-wait) min {(min(ent) - t0) / 1e3:9.2f}  max {(max(ent) - t0) / 1e3:9.2f}")
     for i, ph in enumerate("ABCDE", start=1):
         v = [r[i] for r in rows if r[i]]
         if v:
