@@ -44,20 +44,39 @@ namespace ll128 {
 
 constexpr int kThreads = 512;
 constexpr int kWarps = kThreads / 32;
-constexpr int kLineGranules = 7;  // data granules per 128-byte line
+constexpr int kPairGranules = 15;  // data granules per PAIR of 128-byte lines (15/16 of the bytes)
 constexpr int kLineBytes = 128;
 constexpr unsigned kFull = 0xffffffffu;
 
+// Line pairs. Two consecutive 128-byte lines (an even line and the next) carry
+// 15 granules: in line h (0 or 1) of pair pp, lanes 0-6 hold granules
+// 15 pp + 7 h + 0..6 and lane 7 holds HALF of granule 15 pp + 14 (bytes 0-7
+// in line 0, bytes 8-15 in line 1) followed by the 8-byte flag (the epoch
+// twice). Every line still carries its own flag, so the line-atomicity
+// reading R#25 is unchanged; the flag shrinks from 16 to 8 bytes. The two
+// lines of a pair are always handled by adjacent 8-lane groups of one warp
+// (flat positions 4u + grp with an even number of lines per sub-part, so the
+// line's parity is grp & 1), and the two lane-7s swap halves with one shuffle.
+LANE_HD int64_t lines_of(int64_t su) { return 2 * ceil_div(su, kPairGranules); }
 
-// Lines of a sub-part slot for a chunk whose sub-parts hold at most su granules.
-LANE_HD int64_t lines_of(int64_t su) { return ceil_div(su, kLineGranules); }
+// Granule of a sub-part (or ring part) carried by lane sl of line ln; lane 7
+// of both lines of a pair carries the pair's shared granule 14.
+LANE_HD int32_t line_granule(int32_t ln, int sl) {
+  return kPairGranules * (ln >> 1) + (sl < 7 ? 7 * (ln & 1) + sl : 14);
+}
+// Whether lane sl of line ln stores its granule to the recvbuf (the shared
+// granule once, from the pair's even line).
+LANE_HD bool line_owner(int32_t ln, int sl) { return sl < 7 || (ln & 1) == 0; }
 
 // Lines per parity set for a call: (G-1) L1 + (G-1) L4 slots of N*lu lines
 // per chunk, N L2 + N L3 slots of lu lines per chunk.
 LANE_HD int64_t set_lines(int G, int N, int64_t cap, int64_t lu) { return 2 * (int64_t)G * N * cap * lu; }
 
+// Store this lane's 16 bytes of a line; v = the lane's granule (lane 7: the
+// pair's shared granule, whole: the line's half of it goes with the flag).
 __device__ __forceinline__ void line_store(uint4* line, int sl, const uint4& v, uint32_t ep) {
-  const uint4 w = sl == 7 ? make_uint4(ep, ep, ep, ep) : v;
+  const bool odd = (threadIdx.x >> 3) & 1;  // line parity within its pair (grp & 1)
+  const uint4 w = sl == 7 ? (odd ? make_uint4(v.z, v.w, ep, ep) : make_uint4(v.x, v.y, ep, ep)) : v;
   asm volatile("st.volatile.global.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(line + sl), "r"(w.x), "r"(w.y),
                "r"(w.z), "r"(w.w)
                : "memory");
@@ -76,7 +95,7 @@ __device__ __forceinline__ uint4 line_load(const uint4* line, int sl) {
 // group's line carry this call's epoch? Lane 7 of the group holds the flag
 // words; every lane of the group gets the answer.
 __device__ __forceinline__ bool group_ready(const uint4& v, int sl, uint32_t ep) {
-  const bool f = sl == 7 && v.x == ep && v.y == ep && v.z == ep && v.w == ep;
+  const bool f = sl == 7 && v.z == ep && v.w == ep;
   return __shfl_sync(kFull, f, (int)(threadIdx.x & 31) | 7);
 }
 
@@ -123,11 +142,11 @@ __device__ __noinline__ ll::Got wait_line(const LaneParams& p, const uint4* line
 #endif
 
 // A warp step's U lines per 8-lane group: flat position, the line's
-// pointer(s), whether the line exists (act) and whether this lane holds a data
-// granule of its span (dv).
+// pointer(s), whether the line exists (act: its pair holds data of the span)
+// and whether this lane holds a data granule of the span (dv).
 template <int U>
 struct BatchT {
-  bool act[U], dv[U];
+  bool act[U], dv[U], own[U];  // own: dv and this lane stores the granule to the recvbuf (line_owner)
   int t[U], b[U];
   int32_t ln[U], i[U];  // line in the sub-part, chunk-relative granule (< 2^31: 32-bit, fewer registers)
 };
@@ -139,8 +158,20 @@ __device__ __forceinline__ void fetch_lines(const uint4* const (&ptr)[U], const 
   for (int u = 0; u < U; ++u) v[u] = act[u] ? line_load(ptr[u], sl) : make_uint4(0, 0, 0, 0);
 }
 
+// Warp-collective: lane 7 of each line rebuilds the pair's shared granule
+// from its own half and its partner line's (lane ^ 8).
+template <int U>
+__device__ __forceinline__ void unpack_lines(int sl, uint4 (&v)[U]) {
+  const bool odd = (threadIdx.x >> 3) & 1;
+#pragma unroll
+  for (int u = 0; u < U; ++u) {
+    const uint32_t ox = __shfl_xor_sync(kFull, v[u].x, 8), oy = __shfl_xor_sync(kFull, v[u].y, 8);
+    if (sl == 7) v[u] = odd ? make_uint4(ox, oy, v[u].x, v[u].y) : make_uint4(v[u].x, v[u].y, ox, oy);
+  }
+}
+
 // Warp-collective: wait until every active fetched line carries the epoch
-// (reloading the ones that did not yet).
+// (reloading the ones that did not yet), then unpack the shared granules.
 template <int U>
 __device__ __forceinline__ bool check_lines(const LaneParams& p, const uint4* const (&ptr)[U], const bool (&act)[U],
                                             int sl, uint4 (&v)[U]) {
@@ -151,14 +182,16 @@ __device__ __forceinline__ bool check_lines(const LaneParams& p, const uint4* co
     got[u] = !act[u] || r;
     all = all && got[u];
   }
-  if (__all_sync(kFull, all)) return true;
+  if (!__all_sync(kFull, all)) {
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (!__all_sync(kFull, got[u])) {
-      const ll::Got w = wait_line(p, ptr[u], sl, !got[u], v[u]);
-      if (!w.ok) return false;
-      v[u] = w.v;
-    }
+    for (int u = 0; u < U; ++u)
+      if (!__all_sync(kFull, got[u])) {
+        const ll::Got w = wait_line(p, ptr[u], sl, !got[u], v[u]);
+        if (!w.ok) return false;
+        v[u] = w.v;
+      }
+  }
+  unpack_lines(sl, v);
   return true;
 }
 
@@ -250,13 +283,14 @@ inline Plan128 plan128(int G, int N, int k, int64_t ng, int C, int64_t M, int64_
   return o;
 }
 
-// Lines per parity set allocated at init. A call needs 2*G*N*cap*lu lines;
-// with G*N*su <= CG + G*N and cap*CG <= M + k*CG this is at most
-// 2*(M + k*CG + cap*G*N)/7 + 2*cap*G*N lines; sized for k*CG <= M/4 (which
-// plan128 keeps unless CG is the minimum chunk, covered by the k*cg_min term).
+// Lines per parity set allocated at init. A call needs 2*G*N*cap*lu lines,
+// lu = 2*ceil(su/15) <= 2*su/15 + 2; with G*N*su <= CG + G*N and
+// cap*CG <= M + k*CG this is at most 4*(M + k*CG + cap*G*N)/15 + 4*cap*G*N
+// lines; sized for k*CG <= M/4 (which plan128 keeps unless CG is the minimum
+// chunk, covered by the k*cg_min term).
 inline int64_t set_capacity128(int G, int N, int k, int64_t M, int64_t cg_min) {
   const int64_t chunks = M / cg_min + k + 1;
-  return 2 * ceil_div(M + M / 4 + k * cg_min + chunks * G * N, kLineGranules) + 2 * (int64_t)G * N * chunks + 64;
+  return 2 * (2 * ceil_div(M + M / 4 + k * cg_min + chunks * G * N, kPairGranules) + 2 * (int64_t)G * N * chunks) + 64;
 }
 
 // RING2: the inter-node stage is Alg. 1 (LANE_PHASE2=ring; p.ring2), a separate
@@ -321,8 +355,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
         q.t[u] = (int)(r / (uint32_t)NB);
         const Span up = span(q.t[u], q.b[u]);
         q.act[u] = q.act[u] && q.ln[u] < lines_of(up.len);
-        q.i[u] = q.ln[u] * kLineGranules + sl;
-        q.dv[u] = q.act[u] && sl < kLineGranules && q.i[u] < up.len;
+        q.i[u] = line_granule(q.ln[u], sl);
+        q.dv[u] = q.act[u] && q.i[u] < up.len;
+        q.own[u] = q.dv[u] && line_owner(q.ln[u], sl);
         q.i[u] += (int32_t)up.start;  // granule of the span's chunk-relative part
       }
       if (!f(q)) return false;
@@ -354,8 +389,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
       q.t[u] = (int)(r / (uint32_t)NB);
       const Span up = span(ch, q.t[u], q.b[u]);
       q.act[u] = q.act[u] && q.ln[u] < lines_of(up.len);
-      q.i[u] = q.ln[u] * kLineGranules + sl;
-      q.dv[u] = q.act[u] && sl < kLineGranules && q.i[u] < up.len;
+      q.i[u] = line_granule(q.ln[u], sl);
+      q.dv[u] = q.act[u] && q.i[u] < up.len;
+      q.own[u] = q.dv[u] && line_owner(q.ln[u], sl);
       q.i[u] += (int32_t)up.start;
     }
     return f(ch, q);
@@ -413,10 +449,8 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
       const bool ok = walk(1, 1, widest, [&](const Batch& q) {
         auto up = [&](int x) { return rf_split(gp.len, N, x); };
         auto act = [&](int u, int x) { return q.act[u] && q.ln[u] < lines_of(up(x).len); };
-        auto dv = [&](int u, int x) {
-          return act(u, x) && sl < kLineGranules && q.ln[u] * kLineGranules + sl < up(x).len;
-        };
-        auto gidx = [&](int u, int x) { return ch.g0 + gp.start + up(x).start + q.ln[u] * kLineGranules + sl; };
+        auto dv = [&](int u, int x) { return act(u, x) && line_granule(q.ln[u], sl) < up(x).len; };
+        auto gidx = [&](int u, int x) { return ch.g0 + gp.start + up(x).start + line_granule(q.ln[u], sl); };
         // node sum of ring chunk x at this group's lines (warp-collective)
         auto t1 = [&](int x, uint4 (&out)[U]) -> bool {
           typename O::Acc acc[U];
@@ -449,7 +483,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
         auto deliver = [&](int x, const uint4 (&v)[U]) {  // final lines of ring chunk x: recvbuf + phase 3
 #pragma unroll
           for (int u = 0; u < U; ++u) {
-            if (dv(u, x)) store_out(msg, gidx(u, x), v[u]);
+            if (dv(u, x) && line_owner(q.ln[u], sl)) store_out(msg, gidx(u, x), v[u]);
             if (act(u, x))
               for (int t2 = 1; t2 < G; ++t2) {
                 const int h = (g + t2) % G;
@@ -606,7 +640,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const uint4 f = O::narrow(acc[u]);
-        if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], f);
+        if (q.own[u]) store_out(msg, ch.g0 + q.i[u], f);
         if (q.act[u]) {
           for (int t = 1; t < N; ++t) {
             const int b = (a + t) % N;
@@ -641,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
         if (!get_lines(p, ptr, q.act, sl, v)) return false;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-          if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
+          if (q.own[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
           if (q.act[u]) {
             const int b = (a + 1 + q.t[u]) % N;
             for (int t2 = 1; t2 < G; ++t2) {
@@ -673,7 +707,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
       if (!get_lines(p, ptr, q.act, sl, v)) return false;
 #pragma unroll
       for (int u = 0; u < U; ++u)
-        if (q.dv[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
+        if (q.own[u]) store_out(msg, ch.g0 + q.i[u], v[u]);
       return true;
     });
     if (!ok) return;
@@ -770,8 +804,9 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
     auto pstart = [&](int u, int x) { return (int64_t)x * pb[u] + (x < pr[u] ? x : pr[u]); };
     auto plen = [&](int u, int x) { return pb[u] + (x < pr[u] ? 1 : 0); };
     auto act = [&](int u, int x) { return on[u] && ln[u] < lines_of(plen(u, x)); };
-    auto dv = [&](int u, int x) { return act(u, x) && sl < kLineGranules && ln[u] * kLineGranules + sl < plen(u, x); };
-    auto gidx = [&](int u, int x) { return g0[u] + pstart(u, x) + ln[u] * kLineGranules + sl; };
+    auto dv = [&](int u, int x) { return act(u, x) && line_granule((int32_t)ln[u], sl) < plen(u, x); };
+    auto own = [&](int u, int x) { return dv(u, x) && line_owner((int32_t)ln[u], sl); };
+    auto gidx = [&](int u, int x) { return g0[u] + pstart(u, x) + line_granule((int32_t)ln[u], sl); };
 
     uint4 v[U];
 #pragma unroll
@@ -804,7 +839,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
     // rank r completed part r+1 (the last rp)
 #pragma unroll
     for (int u = 0; u < U; ++u)
-      if (dv(u, md(r + 1))) store_out(msg, gidx(u, md(r + 1)), v[u]);
+      if (own(u, md(r + 1))) store_out(msg, gidx(u, md(r + 1)), v[u]);
     // allgather loop (P L190-203)
     for (int s = 0; s < P - 1; ++s) {
       const int sp = md(r + 1 - s), rp = md(r - s);
@@ -824,7 +859,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
       for (int u = 0; u < U; ++u)
         if (a[u]) {
           v[u] = w[u];
-          if (dv(u, rp)) store_out(msg, gidx(u, rp), v[u]);
+          if (own(u, rp)) store_out(msg, gidx(u, rp), v[u]);
         }
     }
   }

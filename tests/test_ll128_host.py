@@ -92,4 +92,5 @@ def test_plans_fit_and_cover_in_the_ll128_range(N, G):
                 assert p["cap"] >= k * 1 and p["cap"] * p["cg"] >= ng, ctx  # the chunks cover the message
                 assert p["cap"] >= k * (-(-slice0 // p["cg"])) - k, ctx
                 su = -(-(-(-p["cg"] // G)) // N)
-                assert p["lu"] * 7 >= su > (p["lu"] - 1) * 7, ctx  # lines cover the largest sub-part
+                # line pairs of 15 granules cover the largest sub-part, no spare pair
+                assert p["lu"] % 2 == 0 and p["lu"] // 2 * 15 >= su > (p["lu"] // 2 - 1) * 15, ctx
