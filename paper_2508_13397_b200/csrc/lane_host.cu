@@ -100,7 +100,7 @@ struct lane_comm_s {
   int chunks_per_cta = 4;
   int direct_mode = 2;     // LANE_DIRECT: registered multi-GPU job set (2 push, 3 pull-all, 4 pull-push, 0 staged)
   int direct_emu = 1;      // LANE_DIRECT in emulated mode (1 direct-pull default)
-  int pdl = 1;             // LANE_PDL: multi-GPU launches with programmatic stream serialization
+  int pdl = 0;             // LANE_PDL=1: multi-GPU launches with programmatic stream serialization
   bool emu_handshake = false;  // LANE_EMU_HANDSHAKE=1 (tests): start/end handshake in emulated mode
   int sig_skew = -1;       // LANE_EMU_SIG_SKEW_RANK (tests): that emulated rank publishes a wrong signature
   int ctas_total = 0;      // LANE_CTAS_TOTAL: simple-protocol CTAs per GPU (multi-GPU)
@@ -362,7 +362,9 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     const char* p2 = getenv("LANE_PHASE2");
     c->phase2_ring = p2 && strcmp(p2, "ring") == 0;
   }
-  c->pdl = env_i64("LANE_PDL", 1) != 0;
+  // PDL is opt-in: it hides the launch gap in a microbenchmark (tools/launch_micro.cu) but measured
+  // no gain in the allreduce and cost ~2% at 1 GiB on 1x4 / 4x1 (profiles/r02_pdl_ab_p4.txt)
+  c->pdl = env_i64("LANE_PDL", 0) != 0;
   c->direct_mode = (int)env_i64("LANE_DIRECT", 2);
   if (c->direct_mode != 0 && c->direct_mode != 3 && c->direct_mode != 4) c->direct_mode = 2;  // 1 (pull): emulated only
   c->direct_emu = (int)env_i64("LANE_DIRECT", 1);
@@ -727,10 +729,11 @@ bool a2_plan(lane_comm_t c, int64_t ng, Plan* pl) {
 }
 
 // One kernel launch of a call. Emulated: cooperative (every CTA of every
-// rank co-resident). Multi-GPU: with programmatic stream serialization
-// (LANE_PDL, default on) so the grid is scheduled while the previous grid in
-// the stream drains; every kernel starts with pdl_enter() (lane_kernels.cuh),
-// which waits for that grid's completion before its first memory access.
+// rank co-resident). Multi-GPU: plain, or with programmatic stream
+// serialization (LANE_PDL=1) so the grid is scheduled while the previous grid
+// in the stream drains; every kernel starts with pdl_enter() (lane_kernels.cuh),
+// which waits for that grid's completion before its first memory access (a
+// no-op without PDL).
 cudaError_t launch_kernel(lane_comm_t c, const void* fn, dim3 grid, dim3 block, void** args, size_t smem,
                           cudaStream_t s) {
   if (c->emulated) return cudaLaunchCooperativeKernel(fn, grid, block, args, smem, s);
