@@ -185,6 +185,27 @@ def test_ll128_cta_counts_and_sizes(ctas, monkeypatch):
     assert emu(2, 4, 1).protocol((4 << 20) + 4, "float32") == "simple"  # beyond the LL128 capacity
 
 
+@pytest.mark.parametrize("N,G", [(1, 2), (2, 2), (2, 4), (8, 1)])
+@pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
+def test_ll128_line_pair_positions(N, G, dtype, monkeypatch):
+    """LL128 line pairs (15 granules per two lines, the pair's shared granule
+    split across the two lane-7s): 40 consecutive ragged counts per layout,
+    so the message's partial last granule, the sub-part ends and the chunk
+    ends land on every position of a pair (0..14, including the shared
+    granule 14) and sub-parts shorter than one pair occur; bit-exact vs the
+    oracle on every rank."""
+    monkeypatch.setenv("LANE_PROTO", "ll128")
+    q = 4 if dtype == "float32" else 8
+    P = N * G
+    for k in (1, 2):
+        e = emu(N, G, k)
+        for m in range(40):
+            n = q * (15 * P * 3 + 7 * m) + (m % q) + 1  # granules: 45P + 7m (+ a partial one)
+            assert e.protocol(n, dtype) == "ll128"
+            xs = si.generate_all(dtype, "signed", 300 + m, P, n)
+            assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"ll128 pairs {N}x{G} k={k} n={n}")
+
+
 def test_multi_round_and_chunk_sizes():
     import paper_2508_13397_b200 as lane
     old = (os.environ.get("LANE_ROUND_BYTES"), os.environ.get("LANE_CHUNK_BYTES"))
