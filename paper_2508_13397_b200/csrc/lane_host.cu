@@ -319,9 +319,11 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
     return fail(c, LANE_ERR_INVALID_ARG, "LANE_THREADS must be a multiple of 32 in [64, 512]");
   c->ctas_per_group = (int)env_i64("LANE_CTAS_PER_GROUP", 0);
   c->round_cap = env_i64("LANE_ROUND_BYTES", (int64_t)1 << 30) / 16;
-  // Largest pipeline chunk: 1 MiB chunks cost the all-to-all layouts up to 10% at 1 GiB (1x4 615 vs
-  // 690 GB/s with 256 KiB; 4x1 652 vs 683 with 512 KiB; 2x2 neutral: profiles/r02_chunk_budget_p4.txt)
-  c->cg_max = env_i64("LANE_CHUNK_BYTES", N == 1 ? (256 << 10) : (512 << 10)) / 16;
+  // Largest pipeline chunk. Multi-GPU: 1 MiB chunks cost the all-to-all layouts up to 10% at 1 GiB
+  // (1x4 615 vs 690 GB/s with 256 KiB; 4x1 652 vs 683 with 512 KiB; 2x2 neutral:
+  // profiles/r02_chunk_budget_p4.txt). Emulated (HBM-bound, every rank in one launch): 1 MiB
+  // (512 KiB chunks cost the N = 1 bench 8%: 4.30 -> 4.66 ms).
+  c->cg_max = env_i64("LANE_CHUNK_BYTES", emulated ? (1 << 20) : (N == 1 ? (256 << 10) : (512 << 10))) / 16;
   c->cg_min = env_i64("LANE_MIN_CHUNK_BYTES", 128 << 10) / 16;
   c->chunks_per_cta = (int)env_i64("LANE_CHUNKS_PER_CTA", 4);
   if (c->chunks_per_cta < 1) c->chunks_per_cta = 1;
