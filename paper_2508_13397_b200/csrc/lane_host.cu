@@ -137,6 +137,8 @@ struct lane_comm_s {
   uint32_t* err_host = nullptr;  // mapped pinned word
   uint32_t* err_dev = nullptr;
   uint32_t* abort_dev = nullptr;
+  uint32_t* claims = nullptr;  // chunk-claim counters (lane_plan.h claim_index)
+  int dyn = -1;                // LANE_DYN_CHUNKS: TMA engine CTAs claim chunks dynamically (1), statically (0), auto (-1)
   uint64_t timeout_ns = 0;
   uint64_t* trace = nullptr;  // LANE_TRACE=1: kTraceWords per CTA of the last launch
   int trace_ctas = 0;
@@ -369,6 +371,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   // PDL is opt-in: it hides the launch gap in a microbenchmark (tools/launch_micro.cu) but measured
   // no gain in the allreduce and cost ~2% at 1 GiB on 1x4 / 4x1 (profiles/r02_pdl_ab_p4.txt)
   c->pdl = env_i64("LANE_PDL", 0) != 0;
+  c->dyn = (int)env_i64("LANE_DYN_CHUNKS", -1);
   c->direct_mode = (int)env_i64("LANE_DIRECT", 2);
   if (c->direct_mode != 0 && c->direct_mode != 3 && c->direct_mode != 4) c->direct_mode = 2;  // 1 (pull): emulated only
   c->direct_emu = (int)env_i64("LANE_DIRECT", 1);
@@ -459,6 +462,8 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   LANE_CUDA(c, cudaHostGetDevicePointer(&c->err_dev, c->err_host, 0));
   LANE_CUDA(c, cudaMalloc(&c->abort_dev, 64));
   LANE_CUDA(c, cudaMemset(c->abort_dev, 0, 64));
+  LANE_CUDA(c, cudaMalloc(&c->claims, lane::kClaimWords * 4));
+  LANE_CUDA(c, cudaMemset(c->claims, 0, lane::kClaimWords * 4));
   if (env_i64("LANE_TRACE", 0)) {
     const size_t nt = (size_t)(c->max_coresident > c->ll_coresident ? c->max_coresident : c->ll_coresident);
     LANE_CUDA(c, cudaMalloc(&c->trace, nt * lane::kTraceWords * 8));
@@ -654,6 +659,8 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.fcap = c->chunk_cap;
   p.sig_skew = c->sig_skew;
   p.releasers = c->releasers;
+  p.claims = c->claims;
+  p.dyn = c->dyn > 0 ? 1 : 0;
   return p;
 }
 
@@ -823,6 +830,11 @@ int launch_rounds(lane_comm_t c, LaneParams& p, const Plan& pl, int dtype, cudaS
     p.cap = lane::round_chunks(p.round_len, c->k, p.cg);
     // the simple protocol's flag arrays hold chunk_cap chunks (the LL plan checked its inboxes itself)
     if (pl.ll == kSimple && p.cap > c->chunk_cap) return fail(c, LANE_ERR_INVALID_ARG, "internal: chunk capacity");
+    // Chunk claims (LANE_DYN_CHUNKS): auto = dynamic on real peers when a CTA has at least 6 chunks
+    // of the round — there per-SM push rates differ by up to 2x and the fast CTAs take more chunks
+    // (1 GiB +3%, box-independent); with fewer chunks the static round-robin is 1-3% faster
+    // (profiles/r02_dyn_chunks_ab_p4.txt). Emulated: static unless forced.
+    if (c->dyn < 0) p.dyn = (!c->emulated && p.cap >= 6 * (int64_t)c->k * p.C) ? 1 : 0;
     p.epoch = ++c->epoch;
     const bool tma = c->engine == 1;
     dim3 grid((unsigned)(nlocal * c->k * p.C));
@@ -1471,6 +1483,7 @@ void release(lane_comm_t c) {
     }
   }
   if (c->abort_dev) cudaFree(c->abort_dev);
+  if (c->claims) cudaFree(c->claims);
   if (c->trace) cudaFree(c->trace);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;

@@ -70,11 +70,20 @@ __device__ __forceinline__ void pdl_enter() {
 
 __device__ __forceinline__ uint64_t globaltimer_ns();
 
-// Every kernel of a comm starts here (PDL wait; pdl_enter). Returns the time
-// the CTA began, before the wait (trace: how early PDL dispatched it).
-__device__ __forceinline__ uint64_t launch_prologue(const LaneParams&) {
+// Zero the chunk-claim counters of the next launch's parity (lane_plan.h).
+__device__ __noinline__ void claims_reset(const LaneParams& p, int rank) {
+  const int par = (int)((p.epoch + 1u) & 1u);
+  for (int l = threadIdx.x; l < p.k; l += blockDim.x) p.claims[claim_index(rank, par, l)] = 0u;
+}
+
+// Every kernel of a comm starts here: PDL wait (pdl_enter), then the first CTA
+// of each local rank zeroes the next launch's chunk-claim counters. Returns
+// the time the CTA began, before the wait (trace: how early PDL dispatched it).
+__device__ __forceinline__ uint64_t launch_prologue(const LaneParams& p) {
   const uint64_t t = globaltimer_ns();
   pdl_enter();
+  const int per_rank = p.k * p.C;
+  if (p.claims != nullptr && blockIdx.x % per_rank == 0) claims_reset(p, p.rank0 + (int)(blockIdx.x / per_rank));
   return t;
 }
 

@@ -100,7 +100,18 @@ struct LaneParams {
   int64_t ll_slot_u;    // LL protocol: granules per sub-part slot (L2, L3), per set
   int64_t ll_set;       // LL protocol: granules per parity set (both kernels agree)
   int ring2;            // LL lane kernel: 1 = ring inter-node stage (LANE_PHASE2=ring)
+  int dyn;              // TMA engine: 1 = CTAs claim chunks from a per-(rank, slice) counter (LANE_DYN_CHUNKS)
+  uint32_t* claims;     // those counters (claim_index), zeroed one launch ahead by every kernel
 };
+
+// Chunk-claim counters: one per (rank, parity set = epoch & 1, slice), 32 bytes
+// apart. Every launch of a comm (any kernel) zeroes the NEXT launch's parity
+// (launch_prologue); the next launch starts only after this one completed
+// (stream order), so it finds them zero whatever protocol ran in between.
+LANE_HD int64_t claim_index(int rank, int par, int l) {
+  return (((int64_t)rank * 2 + par) * LANE_MAX_PROCS_PER_GPU + l) * 8;
+}
+constexpr int64_t kClaimWords = (int64_t)LANE_MAX_RANKS * 2 * LANE_MAX_PROCS_PER_GPU * 8;
 
 // Trace record layout (kTraceWords uint64 per CTA, nanoseconds unless noted).
 enum TraceField {

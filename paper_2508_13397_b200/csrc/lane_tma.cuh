@@ -66,7 +66,7 @@ constexpr int kConsumers = 32 * kConsumerWarps;
 constexpr int kMaxSrc = LANE_MAX_RANKS;
 constexpr int kRelSlots = 16;  // release records in flight between storer and releaser
 constexpr int kJobCacheBytes = 5 * 576;  // producer's next job of every phase
-constexpr int kProdStateBytes = 192;     // producer's per-phase cursors (ProdState)
+constexpr int kProdStateBytes = 448;     // producer's per-phase cursors and claim ring (ProdState)
 constexpr int kSmemBytes = kStages * kStageBytes + 2 * kStages * 8 + kStages * 320 + kRelSlots * 136 + 256 +
                            kJobCacheBytes + kProdStateBytes;
 
@@ -494,8 +494,12 @@ __device__ __forceinline__ void publish_release(RelRing* ring, RelRec* rel_rec, 
 
 // The producer's per-phase cursors, in shared memory: they are indexed by the
 // picked phase (a run-time value), which in registers would be a stack array.
+constexpr int kClaimRing = 32;  // claimed chunks held by a CTA's producer (dynamic claims)
+
 struct ProdState {
-  int64_t cur[5];  // next chunk (of this CTA) per phase
+  int64_t cur[5];  // next chunk (ordinal among this CTA's chunks) per phase
+  int64_t chunk[kClaimRing];  // dynamic claims: chunk of ordinal x at [x % kClaimRing]
+  int64_t nclaimed;           // dynamic claims: ordinals claimed so far
   int nj[5];       // jobs per chunk per phase
   int prev[5];     // previous active phase
   int sub[5];      // next job within the chunk
@@ -681,6 +685,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     int* const sub = ps->sub;
     int* const wpos = ps->wpos;  // flags of jobs[ph] already seen set
     int* const have = ps->have;  // jobs[ph] (shared memory): next job of every phase, built once per job
+    int first = -1;  // first active phase: the one that takes a new chunk
     for (int ph = 0, pa = -1; ph < 5; ++ph) {
       nj[ph] = njobs(x, ph);
       cur[ph] = nj[ph] > 0 ? 0 : m;  // inactive phases are "done"
@@ -688,9 +693,27 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       prev[ph] = pa;
       wpos[ph] = 0;
       have[ph] = 0;
-      if (nj[ph] > 0) pa = last = ph;
+      if (nj[ph] > 0) {
+        pa = last = ph;
+        if (first < 0) first = ph;
+      }
     }
     const int64_t window = 6;
+    // Chunks of this CTA. Static: j, j+C, ... (m of them). Dynamic (p.dyn):
+    // claimed one at a time from the rank's per-slice counter when the first
+    // active phase needs a new chunk (within the window), the next claim's
+    // atomic already in flight; a CTA on a fast SM ends up with more chunks.
+    // Deadlock-free as the static schedule: every rank claims in increasing
+    // chunk order, a claimed chunk's first phase never waits (A) or waits only
+    // on peers' earlier phases of the same chunk, and the lowest unfinished
+    // chunk is claimed on every rank.
+    const bool dyn = p.dyn != 0;
+    unsigned* const ctr = dyn ? p.claims + claim_index(x.rank, (int)(p.epoch & 1u), l) : nullptr;
+    unsigned pending = dyn ? atomicAdd(ctr, 1u) : 0u;
+    bool claim_done = !dyn;
+    ps->nclaimed = 0;
+    auto limit = [&]() -> int64_t { return dyn ? ps->nclaimed : m; };
+    auto chunk_of = [&](int64_t ord) -> int64_t { return dyn ? ps->chunk[ord % kClaimRing] : j + ord * p.C; };
     int64_t k = 0;  // global tile counter
     bool ok = true;
     // Start-of-call handshake (every simple-protocol call on real peers): a
@@ -750,12 +773,32 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       int pick = -1;
       bool any_left = false;
       for (int ph = 0; ph < 5 && pick < 0; ++ph) {
-        if (cur[ph] >= m) continue;
+        if (nj[ph] == 0) continue;
+        if (cur[ph] >= limit()) {
+          if (claim_done || ph != first) {
+            if (!claim_done) any_left = true;  // later phases wait for the next claim
+            continue;
+          }
+          if (last != first && cur[first] - cur[last] >= window) {
+            any_left = true;
+            continue;
+          }
+          const unsigned c = pending;  // take the claim in flight, start the next
+          if ((int64_t)c >= nc) {
+            claim_done = true;
+            continue;
+          }
+          pending = atomicAdd(ctr, 1u);
+          ps->chunk[ps->nclaimed % kClaimRing] = (int64_t)c;
+          ++ps->nclaimed;
+        }
         any_left = true;
         if (prev[ph] >= 0 && cur[ph] >= cur[prev[ph]]) continue;  // previous phase not issued yet
-        if (ph == 0 && last >= 0 && last != 0 && cur[0] - cur[last] >= window) continue;
+        // the window: phase A (static; as before) or the first active phase (dynamic, which also
+        // bounds the claim ring) runs at most `window` chunks ahead of the last phase
+        if (ph == first && (first == 0 || dyn) && last != first && cur[first] - cur[last] >= window) continue;
         if (!have[ph]) {
-          make_job(x, ph, chunk_geo(p, cb, sl, j + cur[ph] * p.C), sub[ph], jobs[ph]);
+          make_job(x, ph, chunk_geo(p, cb, sl, chunk_of(cur[ph])), sub[ph], jobs[ph]);
           have[ph] = 1;
           wpos[ph] = 0;
         }

@@ -49,14 +49,18 @@ def main():
     t0 = time.time()
     maxb = max(counts) * 4
     cases = [(N, G, k, pr) for (N, G) in layouts(P) for k in ks
-             for pr in ("simple", "pull", "pullpush", "ll", "ll128", "ring2", "ring2_128")]
+             for pr in ("simple", "dyn", "pull", "pullpush", "ll", "ll128", "ring2", "ring2_128")]
     if args.quick:  # the standard multi-PPG approach at PPG 16 (Alg. 1 per slice, P L431), both protocols
         cases += [(1, P, 16, "ll"), (1, P, 16, "ll128")]
     for N, G, k, proto in cases:
         if True:
             # ll / ll128: every call that fits that protocol's inboxes
-            os.environ["LANE_PROTO"] = {"simple": "simple", "pull": "simple", "pullpush": "simple", "ll128": "ll128",
-                                        "ring2_128": "ll128"}.get(proto, "ll")
+            os.environ["LANE_PROTO"] = {"simple": "simple", "dyn": "simple", "pull": "simple", "pullpush": "simple",
+                                        "ll128": "ll128", "ring2_128": "ll128"}.get(proto, "ll")
+            if proto == "dyn":  # chunks claimed dynamically (forced; the default is by chunks per CTA)
+                os.environ["LANE_DYN_CHUNKS"] = "1"
+            else:
+                os.environ.pop("LANE_DYN_CHUNKS", None)
             # registered job set: push / pull-all / pull-push
             os.environ["LANE_DIRECT"] = {"pull": "3", "pullpush": "4"}.get(proto, "2")
             if proto.startswith("ring2"):  # the lane method with Alg. 1 as its inter-node stage

@@ -48,7 +48,8 @@ def emu(N, G, k):
                                                         "LANE_LL_MAX_BYTES", "LANE_PHASE2", "LANE_RING_CHUNK_BYTES",
                                                         "LANE_LL128_MIN_BYTES", "LANE_LL128_THRESHOLD_BYTES",
                                                         "LANE_LL128_MAX_BYTES", "LANE_DIRECT", "LANE_STORE",
-                                                        "LANE_EMU_HANDSHAKE", "LANE_BULK_MIN_BYTES"))
+                                                        "LANE_EMU_HANDSHAKE", "LANE_BULK_MIN_BYTES",
+                                                        "LANE_DYN_CHUNKS"))
     if key not in _COMMS:
         while len(_COMMS) >= 4:  # every emulated comm holds P ranks' scratch: keep a few
             _COMMS.pop(next(iter(_COMMS))).close()
@@ -90,8 +91,9 @@ def set_mode(mode, monkeypatch):
     0 = staged (the unregistered job set) — with suffix 'b' = TMA bulk stores
     (LANE_STORE=bulk: what every multi-GPU call >= LANE_BULK_MIN_BYTES runs)
     and 'h' = the start/end handshake with the call signature that every
-    multi-GPU simple-protocol call runs (LANE_EMU_HANDSHAKE=1); or the LL /
-    LL128 protocols."""
+    multi-GPU simple-protocol call runs (LANE_EMU_HANDSHAKE=1), 'd' = chunks
+    claimed dynamically by the CTAs (LANE_DYN_CHUNKS=1); or the LL / LL128
+    protocols."""
     if mode in ("ll", "ll128"):
         monkeypatch.setenv("LANE_PROTO", mode)
         return
@@ -101,11 +103,14 @@ def set_mode(mode, monkeypatch):
         monkeypatch.setenv("LANE_STORE", "bulk")
     if "h" in mode:
         monkeypatch.setenv("LANE_EMU_HANDSHAKE", "1")
+    if "d" in mode:
+        monkeypatch.setenv("LANE_DYN_CHUNKS", "1")
 
 
 @pytest.mark.parametrize("N,G", LAYOUTS)
 @pytest.mark.parametrize("dtype", ["int32", "float32", "bfloat16"])
-@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "0hb", "2hb", "3hb", "4hb", "2h", "1b"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "0hb", "2hb", "3hb", "4hb", "2h", "1b",
+                                  "1d", "2hbd", "0hbd", "4hbd"])
 def test_parity_layouts(N, G, dtype, mode, monkeypatch):
     """Every job set / store mode / protocol (set_mode) on every layout, k and
     ragged count, bit-exact vs the oracle."""
@@ -128,13 +133,17 @@ def test_parity_k_sweep_and_full_range(dtype):
         assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"k={k}")
 
 
-@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "mixed", "0hb", "2hb", "3hb", "4hb"])
+@pytest.mark.parametrize("mode", ["1", "2", "3", "4", "0", "ll", "ll128", "mixed", "0hb", "2hb", "3hb", "4hb",
+                                  "mixed-d", "1d"])
 def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
     """Repeated calls of varying sizes reuse scratch, flags (fixed flag stride:
     one index, one meaning across calls), the handshake's control words and
     (LL, LL128) the two inbox parity sets; "mixed" alternates the LL, LL128 and
-    simple protocols between calls."""
-    if mode == "mixed":
+    simple protocols between calls ("mixed-d": with dynamic chunk claims, whose
+    counters every kernel type zeroes one launch ahead)."""
+    if mode.startswith("mixed"):
+        if mode == "mixed-d":
+            monkeypatch.setenv("LANE_DYN_CHUNKS", "1")
         monkeypatch.setenv("LANE_LL_THRESHOLD_BYTES", str(64 << 10))
         monkeypatch.setenv("LANE_LL128_MIN_BYTES", str(64 << 10))
         monkeypatch.setenv("LANE_LL128_THRESHOLD_BYTES", str(1 << 20))
@@ -147,7 +156,7 @@ def test_inplace_and_repeated_calls_epoch_reuse(mode, monkeypatch):
         xs = si.generate_all(dtype, "signed", 100 + it, 8, n)
         got = run(N, G, k, dtype, xs, inplace=bool(it % 2))
         assert_parity(got, xs, N, G, dtype, f"iter {it}")
-    if mode == "mixed":
+    if mode.startswith("mixed"):
         e = emu(N, G, k)
         assert e.protocol(5000, "float32") == "ll" and e.protocol(1 << 16, "float32") == "ll128"
         assert e.protocol(1 << 20, "float32") == "simple"
@@ -478,7 +487,7 @@ def test_ring_parity_ppg_8_16(proto, k, monkeypatch):
                 assert np.array_equal(bits(o), bits(ref)), f"ring P=8 k={k} {dtype} n={n} rank {p}"
 
 
-@pytest.mark.parametrize("mode", ["1", "0hb", "2hb", "3hb", "4hb", "2h"])
+@pytest.mark.parametrize("mode", ["1", "0hb", "2hb", "3hb", "4hb", "2h", "1d", "2hbd"])
 @pytest.mark.parametrize("dtype", ["float32", "bfloat16"])
 def test_whole_buffer_16mib_job_sets(mode, dtype, monkeypatch):
     """Every simple-protocol job set at 16 MiB per rank + a ragged tail (the
