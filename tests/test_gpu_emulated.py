@@ -49,7 +49,8 @@ def emu(N, G, k):
                                                         "LANE_LL128_MIN_BYTES", "LANE_LL128_THRESHOLD_BYTES",
                                                         "LANE_LL128_MAX_BYTES", "LANE_DIRECT", "LANE_STORE",
                                                         "LANE_EMU_HANDSHAKE", "LANE_BULK_MIN_BYTES",
-                                                        "LANE_DYN_CHUNKS"))
+                                                        "LANE_DYN_CHUNKS", "LANE_CTAS_PER_GROUP",
+                                                        "LANE_MIN_CHUNK_BYTES"))
     if key not in _COMMS:
         while len(_COMMS) >= 4:  # every emulated comm holds P ranks' scratch: keep a few
             _COMMS.pop(next(iter(_COMMS))).close()
@@ -232,6 +233,26 @@ def test_multi_round_and_chunk_sizes():
                 os.environ.pop(key, None)
             else:
                 os.environ[key] = v
+
+
+@pytest.mark.parametrize("mode", ["1d", "2hbd", "0hbd"])
+def test_dynamic_claims_multi_round_few_ctas(mode, monkeypatch):
+    """Chunk claims (LANE_DYN_CHUNKS=1) with many chunks per CTA (3 or 6 CTAs
+    per group; 8 ranks x k = 3 x 6 = 144 co-resident CTAs), k = 1 and 3, several rounds per call (each launch claims from
+    its own zeroed counter), in-place and out-of-place: bit-exact vs the
+    oracle on every rank."""
+    set_mode(mode, monkeypatch)
+    monkeypatch.setenv("LANE_ROUND_BYTES", str(4 << 20))
+    monkeypatch.setenv("LANE_MIN_CHUNK_BYTES", str(16 << 10))
+    monkeypatch.setenv("LANE_CHUNK_BYTES", str(64 << 10))
+    for ctas in ("3", "6"):
+        monkeypatch.setenv("LANE_CTAS_PER_GROUP", ctas)
+        for N, G, k in ((2, 4, 1), (4, 2, 3), (1, 4, 1)):
+            n = (9 << 20) // 4 + 13  # 9 MiB fp32 + a tail -> 3 rounds
+            assert emu(N, G, k).plan(n, "float32")["launches"] == 3
+            xs = si.generate_all("float32", "signed", 77 + k, N * G, n)
+            got = run(N, G, k, "float32", xs, inplace=(ctas == "6"))
+            assert_parity(got, xs, N, G, "float32", f"claims {mode} ctas={ctas} {N}x{G} k={k}")
 
 
 def test_p1_copy_and_zero_count():
