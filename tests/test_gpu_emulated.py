@@ -321,7 +321,8 @@ def test_full_size_sampled_parity(N, G, k, dtype, n):
     """BASELINE sizes, default launch configuration (the one bench.py times):
     inputs filled on the device by the seeded generator; sampled outputs
     (every 4099th element, the last, and +-2 around every chunk/unit
-    boundary) compared bit-exactly with the oracle run on those elements."""
+    boundary) compared bit-exactly with the oracle run on those elements,
+    then every element of every rank against the device canonical-order sum."""
     import torch
     import paper_2508_13397_b200 as lane
     from seeded_inputs import device as sdev
@@ -348,6 +349,12 @@ def test_full_size_sampled_parity(N, G, k, dtype, n):
         for o in outs[1:]:
             assert torch.equal(o.view(torch.int16) if dtype == "bfloat16" else o.view(torch.int32),
                                outs[0].view(torch.int16) if dtype == "bfloat16" else outs[0].view(torch.int32))
+        # and the WHOLE buffer of every rank bit-exact against the canonical-order sum of the
+        # regenerated inputs (bench.verify_whole on the device; pinned to the oracle bit for bit
+        # by tests/test_bench_cpu.py)
+        import bench
+        bad, checked = bench.verify_whole(outs, N, G, dtype, n, 42)
+        assert checked == n * P and bad == 0, (bad, checked)
         c.close()
         del ins, outs
         torch.cuda.empty_cache()
