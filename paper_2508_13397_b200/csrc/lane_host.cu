@@ -342,7 +342,7 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
                                                   : 0);
   }
   // auto range from the P = 2 / P = 4 protocol sweeps (profiles/r01_sizes_protocols_ll128.txt):
-  // LL128 ahead of LL above 1 MiB (2 MiB at P = 2), ahead of simple up to 16 MiB
+  // LL128 capacity (one round of at most this much message uses the LL128 inboxes)
   c->ll128_max = env_i64("LANE_LL128_MAX_BYTES", 32 << 20) / 16;
   if (c->ll128_max < 0) c->ll128_max = 0;
   // Default protocol ranges, from the measured crossovers (profiles/r02_protocol_crossovers.txt,
