@@ -138,7 +138,7 @@ def test_reference_arm_under_torchrun_cpu():
     assert d["config"]["layout"] == "2x1"
 
 
-@pytest.mark.parametrize("gpus", [2, 4])
+@pytest.mark.parametrize("gpus", [2, 4, 8])
 def test_bench_self_launch_without_torchrun_cpu(gpus):
     """``python bench.py --gpus N`` WITHOUT torchrun (no RANK / WORLD_SIZE):
     bench.py launches the N ranks itself through torch.distributed.run on
