@@ -906,6 +906,20 @@ int device_error(lane_comm_t c, const char* when) {
   return fail(c, LANE_ERR_TIMEOUT, std::string("comm: a device-side wait timed out") + when);
 }
 
+// CUDA graph capture is refused: every call bakes its epoch (the generation
+// of its flags and inbox parity set) into its launch parameters, so a
+// replayed graph would find the flags of its previous replay already set and
+// read stale data instead of waiting.
+int check_not_capturing(lane_comm_t c, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  const cudaError_t e = cudaStreamIsCapturing(s, &st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamIsCapturing");
+  if (st != cudaStreamCaptureStatusNone)
+    return fail(c, LANE_ERR_UNSUPPORTED,
+                "stream: CUDA graph capture is not supported (each call's epoch is baked into its launch)");
+  return LANE_OK;
+}
+
 int check_call(lane_comm_t c, uint64_t count, int dtype, int op) {
   if (!c) return LANE_ERR_INVALID_ARG;
   if (dtype < LANE_INT32 || dtype > LANE_BFLOAT16)
@@ -1115,6 +1129,7 @@ int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t cou
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1163,6 +1178,7 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
@@ -1202,6 +1218,7 @@ int lane_allreduce_ring(lane_comm_t c, const void* sendbuf, void* recvbuf, size_
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1227,6 +1244,7 @@ int lane_allreduce_ring_emulated(lane_comm_t c, const void* const* sendbufs, voi
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
@@ -1260,6 +1278,7 @@ int lane_allreduce_approach2(lane_comm_t c, const void* sendbuf, void* recvbuf, 
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1285,6 +1304,7 @@ int lane_allreduce_approach2_emulated(lane_comm_t c, const void* const* sendbufs
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;

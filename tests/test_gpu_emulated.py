@@ -255,6 +255,32 @@ def test_dynamic_claims_multi_round_few_ctas(mode, monkeypatch):
             assert_parity(got, xs, N, G, "float32", f"claims {mode} ctas={ctas} {N}x{G} k={k}")
 
 
+def test_graph_capture_is_refused():
+    """A call on a stream being captured into a CUDA graph returns
+    LANE_ERR_UNSUPPORTED (its epoch would be baked into the graph and a replay
+    would read stale data) without launching anything, and the comm stays
+    usable: the next ordinary call is bit-exact."""
+    import torch
+    import paper_2508_13397_b200 as lane
+    N, G, k, n = 2, 4, 1, 4099
+    e = emu(N, G, k)
+    xs = si.generate_all("float32", "signed", 61, N * G, n)
+    ins = [to_device(x, "float32", "cuda:0") for x in xs]
+    outs = [torch.zeros_like(t) for t in ins]
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(s):
+        g.capture_begin()
+        try:
+            with pytest.raises(lane.LaneError) as ei:
+                e.allreduce(outs, ins)
+        finally:
+            g.capture_end()
+    assert ei.value.code == -2 and "capture" in str(ei.value)
+    assert_parity(run(N, G, k, "float32", xs), xs, N, G, "float32", "after a refused capture")
+
+
 def test_p1_copy_and_zero_count():
     xs = si.generate_all("float32", "signed", 1, 1, 12345)
     assert np.array_equal(run(1, 1, 1, "float32", xs)[0], xs[0])

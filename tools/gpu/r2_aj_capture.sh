@@ -1,0 +1,5 @@
+# round 2 (aj), 1 GPU: graph-capture refusal test + the 1-GPU tier once more.
+set -x
+O=gpurun_out/r2aj; mkdir -p $O
+timeout 1800 python -m pytest tests -m gpu -q > $O/pytest.txt 2>&1; echo "rc=$?" >> $O/pytest.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.txt 2>&1; echo "rc=$?" >> $O/smoke.txt
