@@ -216,6 +216,20 @@ def test_ll128_line_pair_positions(N, G, dtype, monkeypatch):
             assert_parity(run(N, G, k, dtype, xs), xs, N, G, dtype, f"ll128 pairs {N}x{G} k={k} n={n}")
 
 
+@pytest.mark.parametrize("N,G,dtype,mib", [(2, 4, "float32", 20), (4, 2, "bfloat16", 12), (1, 8, "float32", 10)])
+def test_ll128_default_range_top_p8(N, G, dtype, mib, monkeypatch):
+    """LL128 at the top of its default range on P = 8 layouts (2x4 takes LL128
+    up to 32 MiB, 4x2 too, 1x8 up to 16 MiB), default chunking, a ragged
+    tail: every element of every rank bit-exact vs the oracle."""
+    monkeypatch.setenv("LANE_ROUND_BYTES", str(1 << 30))  # LL protocols run one-round messages only
+    q = 4 if dtype == "float32" else 8
+    n = (mib << 20) * q // 16 + 3
+    e = emu(N, G, 1)
+    assert e.protocol(n, dtype) == "ll128"
+    xs = si.generate_all(dtype, "signed", 4242 + mib, N * G, n)
+    assert_parity(run(N, G, 1, dtype, xs), xs, N, G, dtype, f"ll128 top {N}x{G} {mib} MiB")
+
+
 def test_multi_round_and_chunk_sizes():
     import paper_2508_13397_b200 as lane
     old = (os.environ.get("LANE_ROUND_BYTES"), os.environ.get("LANE_CHUNK_BYTES"))
