@@ -49,7 +49,8 @@ typedef enum { LANE_SUM = 0 } lane_op_t;
 typedef enum {
   LANE_OK = 0,
   LANE_ERR_INVALID_ARG = -1,   /* bad topology/argument; last_error names it   */
-  LANE_ERR_UNSUPPORTED = -2,   /* dtype or op outside the enums; stream capture */
+  LANE_ERR_UNSUPPORTED = -2,   /* dtype or op outside the enums; capture of the
+                                  host-buffer API                              */
   LANE_ERR_CUDA = -3,          /* a CUDA runtime call or launch failed         */
   LANE_ERR_NOT_CONNECTED = -4, /* lane_allreduce before lane_allreduce_open_peers
                                   (resolving an unpublished handle) */
@@ -108,10 +109,15 @@ int lane_allreduce_open_peers(lane_comm_t comm, const void* all_blobs, size_t bl
  * in-place; partial overlap is INVALID_ARG. count == 0 is a no-op. Every
  * rank must call with the same (count, dtype, op) in the same order (MPI
  * collective semantics, P L341). Messages larger than the round capacity are
- * processed in several rounds (kernel launches) inside one call. A stream
- * that is being captured into a CUDA graph is UNSUPPORTED (every call bakes
- * its epoch into its launch, so a replay would read stale data); the same
- * holds for the ring, approach-2 and emulated entry points. */
+ * processed in several rounds (kernel launches) inside one call. The call
+ * may be captured into a CUDA graph (stream capture): from the first
+ * captured call on, the comm takes every launch's epoch (the generation of
+ * its flags and packets) from device memory, so each replay — and every
+ * later eager call — gets a fresh one; every rank must replay its graphs and
+ * make its eager calls in the same order (collective semantics). The same
+ * holds for the ring, approach-2 and emulated entry points; the host-buffer
+ * entry points (lane_allreduce_host, _emulated_host) cannot be captured
+ * (UNSUPPORTED). */
 int lane_allreduce(lane_comm_t comm, const void* sendbuf, void* recvbuf, size_t count,
                    lane_dtype_t dtype, lane_op_t op, void* stream);
 

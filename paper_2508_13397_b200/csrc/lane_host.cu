@@ -138,6 +138,8 @@ struct lane_comm_s {
   uint32_t* err_dev = nullptr;
   uint32_t* abort_dev = nullptr;
   uint32_t* claims = nullptr;  // chunk-claim counters (lane_plan.h claim_index)
+  uint32_t* epoch_dev = nullptr;  // per local rank: next epoch + arrival count (lane_kernels.cuh launch_prologue)
+  int dev_epoch = 0;              // 1 once a call was captured into a CUDA graph (sticky)
   int dyn = -1;                // LANE_DYN_CHUNKS: TMA engine CTAs claim chunks dynamically (1), statically (0), auto (-1)
   uint64_t timeout_ns = 0;
   uint64_t* trace = nullptr;  // LANE_TRACE=1: kTraceWords per CTA of the last launch
@@ -464,6 +466,13 @@ int common_init_impl(lane_comm_t c, int N, int G, int k, int rank, int device, b
   LANE_CUDA(c, cudaMemset(c->abort_dev, 0, 64));
   LANE_CUDA(c, cudaMalloc(&c->claims, lane::kClaimWords * 4));
   LANE_CUDA(c, cudaMemset(c->claims, 0, lane::kClaimWords * 4));
+  {
+    uint32_t init[LANE_MAX_RANKS * 16];
+    memset(init, 0, sizeof(init));
+    for (int r = 0; r < LANE_MAX_RANKS; ++r) init[r * 16] = 1u;  // the first launch's epoch (c->epoch + 1)
+    LANE_CUDA(c, cudaMalloc(&c->epoch_dev, sizeof(init)));
+    LANE_CUDA(c, cudaMemcpy(c->epoch_dev, init, sizeof(init), cudaMemcpyHostToDevice));
+  }
   if (env_i64("LANE_TRACE", 0)) {
     const size_t nt = (size_t)(c->max_coresident > c->ll_coresident ? c->max_coresident : c->ll_coresident);
     LANE_CUDA(c, cudaMalloc(&c->trace, nt * lane::kTraceWords * 8));
@@ -661,6 +670,8 @@ LaneParams base_params(lane_comm_t c, const Plan& pl) {
   p.releasers = c->releasers;
   p.claims = c->claims;
   p.dyn = c->dyn > 0 ? 1 : 0;
+  p.epoch_dev = c->epoch_dev;
+  p.dev_epoch = c->dev_epoch;
   return p;
 }
 
@@ -906,17 +917,28 @@ int device_error(lane_comm_t c, const char* when) {
   return fail(c, LANE_ERR_TIMEOUT, std::string("comm: a device-side wait timed out") + when);
 }
 
-// CUDA graph capture is refused: every call bakes its epoch (the generation
-// of its flags and inbox parity set) into its launch parameters, so a
-// replayed graph would find the flags of its previous replay already set and
-// read stale data instead of waiting.
-int check_not_capturing(lane_comm_t c, cudaStream_t s) {
+// CUDA graph capture. A captured launch would replay the epoch it was captured
+// with, so once a comm sees a capturing stream it switches for good to
+// device-side epochs (LaneParams::dev_epoch; lane_kernels.cuh launch_prologue):
+// every launch, captured or not, takes the next epoch from device memory and
+// advances it there. The device word follows the host counter on every eager
+// launch, so the switch can happen at any call.
+int note_capture(lane_comm_t c, cudaStream_t s) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  const cudaError_t e = cudaStreamIsCapturing(s, &st);
+  if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamIsCapturing");
+  if (st != cudaStreamCaptureStatusNone) c->dev_epoch = 1;
+  return LANE_OK;
+}
+
+// The host-buffer entry points synchronise their staging streams and cannot
+// be captured.
+int refuse_capture(lane_comm_t c, cudaStream_t s) {
   cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
   const cudaError_t e = cudaStreamIsCapturing(s, &st);
   if (e != cudaSuccess) return cuda_fail(c, e, "cudaStreamIsCapturing");
   if (st != cudaStreamCaptureStatusNone)
-    return fail(c, LANE_ERR_UNSUPPORTED,
-                "stream: CUDA graph capture is not supported (each call's epoch is baked into its launch)");
+    return fail(c, LANE_ERR_UNSUPPORTED, "stream: the host-buffer API cannot be captured into a CUDA graph");
   return LANE_OK;
 }
 
@@ -1129,7 +1151,7 @@ int lane_allreduce(lane_comm_t c, const void* sendbuf, void* recvbuf, size_t cou
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1178,7 +1200,7 @@ int lane_allreduce_emulated(lane_comm_t c, const void* const* sendbufs, void* co
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
@@ -1218,7 +1240,7 @@ int lane_allreduce_ring(lane_comm_t c, const void* sendbuf, void* recvbuf, size_
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1244,7 +1266,7 @@ int lane_allreduce_ring_emulated(lane_comm_t c, const void* const* sendbufs, voi
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
@@ -1278,7 +1300,7 @@ int lane_allreduce_approach2(lane_comm_t c, const void* sendbuf, void* recvbuf, 
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbuf, recvbuf, pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = c->rank;
@@ -1304,7 +1326,7 @@ int lane_allreduce_approach2_emulated(lane_comm_t c, const void* const* sendbufs
   st = make_plan(c, count, dtype, &pl);
   if (st != LANE_OK) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if ((st = check_not_capturing(c, s)) != LANE_OK) return st;
+  if ((st = note_capture(c, s)) != LANE_OK) return st;
   if (c->P == 1) return copy_p1(c, sendbufs[0], recvbufs[0], pl, s);
   LaneParams p = base_params(c, pl);
   p.rank0 = 0;
@@ -1386,6 +1408,7 @@ int lane_allreduce_host(lane_comm_t c, const void* host_send, void* host_recv, s
   if (c->emulated) return fail(c, LANE_ERR_INVALID_ARG, "lane_allreduce_host: use lane_allreduce_emulated_host");
   if (count == 0) return LANE_OK;
   if (!host_send || !host_recv) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+  if ((st = refuse_capture(c, static_cast<cudaStream_t>(stream))) != LANE_OK) return st;
   const void* hs[1] = {host_send};
   void* hr[1] = {host_recv};
   return host_pipeline(c, hs, hr, count, dtype, op, static_cast<cudaStream_t>(stream));
@@ -1401,6 +1424,7 @@ int lane_allreduce_emulated_host(lane_comm_t c, const void* const* host_sends,
   if (!host_sends || !host_recvs) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
   for (int r = 0; r < c->P; ++r)
     if (!host_sends[r] || !host_recvs[r]) return fail(c, LANE_ERR_INVALID_ARG, "host buffers: null");
+  if ((st = refuse_capture(c, static_cast<cudaStream_t>(stream))) != LANE_OK) return st;
   return host_pipeline(c, host_sends, host_recvs, count, dtype, op, static_cast<cudaStream_t>(stream));
 }
 
@@ -1504,6 +1528,7 @@ void release(lane_comm_t c) {
   }
   if (c->abort_dev) cudaFree(c->abort_dev);
   if (c->claims) cudaFree(c->claims);
+  if (c->epoch_dev) cudaFree(c->epoch_dev);
   if (c->trace) cudaFree(c->trace);
   if (c->err_host) cudaFreeHost(c->err_host);
   delete c;

@@ -70,20 +70,58 @@ __device__ __forceinline__ void pdl_enter() {
 
 __device__ __forceinline__ uint64_t globaltimer_ns();
 
+// The launch's epoch (the generation of its flags, packets and inbox parity
+// set), set once per CTA by launch_prologue; every device-side use reads it
+// from here (cur_epoch()).
+//  - eager launches: the host's counter (LaneParams::epoch); the first CTA of
+//    each local rank also stores epoch + 1 as the rank's NEXT epoch in device
+//    memory, so the device word always follows the host;
+//  - CUDA graph launches (LaneParams::dev_epoch, sticky once a comm was
+//    captured): a replayed graph carries the epoch it was captured with, so
+//    the launch takes the NEXT epoch from device memory instead, and the last
+//    CTA of the rank to arrive advances it (atomic arrival count,
+//    acquire-release: every CTA read the word before the last one moves it).
+//    Every launch therefore still gets epoch previous + 1 on every rank.
+__shared__ uint32_t g_epoch;
+__device__ __forceinline__ uint32_t cur_epoch() { return g_epoch; }
+
+__device__ __noinline__ uint32_t epoch_from_device(const LaneParams& p, int rank, int per_rank) {
+  uint32_t* const st = p.epoch_dev + (int64_t)rank * 16;
+  uint32_t e, t;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(e) : "l"(st) : "memory");
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(st + 1) : "memory");
+  if ((int)t == per_rank - 1) {  // the last CTA of this rank to read it: advance for the next launch
+    st[1] = 0u;
+    asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(st), "r"(e + 1u) : "memory");
+  }
+  return e;
+}
+
 // Zero the chunk-claim counters of the next launch's parity (lane_plan.h).
 __device__ __noinline__ void claims_reset(const LaneParams& p, int rank) {
-  const int par = (int)((p.epoch + 1u) & 1u);
+  const int par = (int)((cur_epoch() + 1u) & 1u);
   for (int l = threadIdx.x; l < p.k; l += blockDim.x) p.claims[claim_index(rank, par, l)] = 0u;
 }
 
-// Every kernel of a comm starts here: PDL wait (pdl_enter), then the first CTA
-// of each local rank zeroes the next launch's chunk-claim counters. Returns
-// the time the CTA began, before the wait (trace: how early PDL dispatched it).
+// Every kernel of a comm starts here (all threads): PDL wait (pdl_enter), the
+// launch's epoch (g_epoch), then the first CTA of each local rank zeroes the
+// next launch's chunk-claim counters. Returns the time the CTA began, before
+// the wait (trace: how early PDL dispatched it).
 __device__ __forceinline__ uint64_t launch_prologue(const LaneParams& p) {
   const uint64_t t = globaltimer_ns();
   pdl_enter();
   const int per_rank = p.k * p.C;
-  if (p.claims != nullptr && blockIdx.x % per_rank == 0) claims_reset(p, p.rank0 + (int)(blockIdx.x / per_rank));
+  const int rank = p.rank0 + (int)(blockIdx.x / per_rank);
+  if (threadIdx.x == 0) {
+    if (p.dev_epoch) {
+      g_epoch = epoch_from_device(p, rank, per_rank);
+    } else {
+      g_epoch = p.epoch;
+      if (p.epoch_dev != nullptr && blockIdx.x % per_rank == 0) p.epoch_dev[(int64_t)rank * 16] = p.epoch + 1u;
+    }
+  }
+  __syncthreads();
+  if (p.claims != nullptr && blockIdx.x % per_rank == 0) claims_reset(p, rank);
   return t;
 }
 
@@ -236,10 +274,10 @@ __device__ __forceinline__ bool wait_flags(const LaneParams& p, const uint32_t* 
   const int t = threadIdx.x;
   if (t < n && t != skip) {
     const uint32_t* f = flags + idx(t);
-    if ((int32_t)(ld_acquire_sys(f) - p.epoch) < 0) {
+    if ((int32_t)(ld_acquire_sys(f) - cur_epoch()) < 0) {
       uint64_t t0 = globaltimer_ns();
       for (uint32_t it = 1;; ++it) {
-        if ((int32_t)(ld_acquire_sys(f) - p.epoch) >= 0) break;
+        if ((int32_t)(ld_acquire_sys(f) - cur_epoch()) >= 0) break;
         if ((it & 63u) == 0) {
           if (*reinterpret_cast<volatile uint32_t*>(p.abort_flag)) {
             fail = 1;
@@ -293,7 +331,7 @@ __global__ void __launch_bounds__(512, 1) lane_allreduce_kernel(const __grid_con
   const int G = p.G, N = p.N;
   const int a = rank / G, g = rank % G;
   const RankMem& me = p.rk[rank];
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int tid = threadIdx.x, nthr = blockDim.x;
 
   Msg msg;

@@ -81,7 +81,7 @@ __device__ __noinline__ Got ll_wait_slow(const LaneParams& p, const uint64_t* li
   Got r;
   r.ok = 0;
   for (uint32_t it = 1;; ++it) {
-    if (ll_try(line, p.epoch, r.v)) {
+    if (ll_try(line, cur_epoch(), r.v)) {
       r.ok = 1;
       return r;
     }
@@ -98,7 +98,7 @@ __device__ __noinline__ Got ll_wait_slow(const LaneParams& p, const uint64_t* li
 }
 
 __device__ __forceinline__ bool ll_wait(const LaneParams& p, const uint64_t* line, uint4& v) {
-  if (ll_try(line, p.epoch, v)) return true;
+  if (ll_try(line, cur_epoch(), v)) return true;
   const Got r = ll_wait_slow(p, line);
   v = r.v;
   return r.ok != 0;
@@ -119,7 +119,7 @@ __device__ __forceinline__ bool ll_sum(const LaneParams& p, int n, int own, cons
     for (int u = 0; u < B; ++u) {
       const int s = s0 + u;
       hit[u] = true;
-      if (s < n && s != own) hit[u] = ll_try(line(s), p.epoch, v[u]);
+      if (s < n && s != own) hit[u] = ll_try(line(s), cur_epoch(), v[u]);
     }
 #pragma unroll
     for (int u = 0; u < B; ++u) {
@@ -171,7 +171,7 @@ LANE_HD int64_t set_granules(int G, int N, int64_t slot_g, int64_t slot_u) {
 }
 
 __device__ __forceinline__ uint64_t* set_base(const LaneParams& p, const RankMem& m) {
-  return reinterpret_cast<uint64_t*>(m.ll) + (int64_t)(p.epoch & 1u) * p.ll_set * 4;
+  return reinterpret_cast<uint64_t*>(m.ll) + (int64_t)(cur_epoch() & 1u) * p.ll_set * 4;
 }
 
 __device__ __forceinline__ Inbox inbox_of(const LaneParams& p, const RankMem& m) {
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ll_kernel(c
   const int64_t j = blockIdx.x % p.C;
   const int G = p.G, N = p.N;
   const int a = rank / G, g = rank % G;
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int tid = threadIdx.x;
   constexpr int nthr = kThreads;
 
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_ring_ll_ker
   const int l = (int)(blockIdx.x % per_rank) / p.C;
   const int64_t j = blockIdx.x % p.C;
   const int P = p.P;
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int tid = threadIdx.x;
   constexpr int nthr = kThreads;
 
@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(kThreads, LANE_LL_MIN_BLOCKS) lane_a2_ll_kerne
   const int64_t j = blockIdx.x % p.C;
   const int G = p.G, N = p.N;
   const int a = rank / G, g = rank % G;
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int tid = threadIdx.x;
   constexpr int nthr = kThreads;
 

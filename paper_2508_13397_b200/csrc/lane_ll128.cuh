@@ -111,7 +111,7 @@ __device__ __noinline__ ll::Got wait_line(const LaneParams& p, const uint4* line
   res.ok = 0;
   for (uint32_t it = 1;; ++it) {
     if (!got) v = line_load(line, sl);
-    const bool r = group_ready(v, sl, p.epoch);
+    const bool r = group_ready(v, sl, cur_epoch());
     got = got || r;
     if (__all_sync(kFull, got)) {
       res.v = v;
@@ -178,7 +178,7 @@ __device__ __forceinline__ bool check_lines(const LaneParams& p, const uint4* co
   bool got[U], all = true;
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const bool r = group_ready(v[u], sl, p.epoch);
+    const bool r = group_ready(v[u], sl, cur_epoch());
     got[u] = !act[u] || r;
     all = all && got[u];
   }
@@ -248,7 +248,7 @@ struct Inbox128 {
 // p.ll_set = lines per parity set (stride); p.cap chunks, lu from p.su.
 __device__ __forceinline__ Inbox128 inbox_of(const LaneParams& p, const RankMem& m) {
   Inbox128 b;
-  b.base = reinterpret_cast<uint4*>(m.ll128) + (int64_t)(p.epoch & 1u) * p.ll_set * 8;
+  b.base = reinterpret_cast<uint4*>(m.ll128) + (int64_t)(cur_epoch() & 1u) * p.ll_set * 8;
   b.y = layout128(p.G, p.N, p.cap, lines_of(p.su));
   return b;
 }
@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ll128_kernel(const __grid_co
   const int64_t j = blockIdx.x % p.C;
   const int G = p.G, N = p.N;
   const int a = rank / G, g = rank % G;
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 3, sl = threadIdx.x & 7;
   const int64_t lu = lines_of(p.su);
   const uint4 z = make_uint4(0, 0, 0, 0);
@@ -759,7 +759,7 @@ __global__ void __launch_bounds__(kThreads, 1) lane_ring_ll128_kernel(const __gr
   const int l = (int)(blockIdx.x % per_rank) / p.C;
   const int j = (int)(blockIdx.x % p.C);
   const int P = p.P;
-  const uint32_t ep = p.epoch;
+  const uint32_t ep = cur_epoch();
   const int warp = threadIdx.x >> 5, grp = (threadIdx.x & 31) >> 3, sl = threadIdx.x & 7;
   const int64_t lp = lines_of(p.sg);  // p.sg = ceil(cg / P): longest ring part
   const uint4 z = make_uint4(0, 0, 0, 0);

@@ -102,6 +102,8 @@ struct LaneParams {
   int ring2;            // LL lane kernel: 1 = ring inter-node stage (LANE_PHASE2=ring)
   int dyn;              // TMA engine: 1 = CTAs claim chunks from a per-(rank, slice) counter (LANE_DYN_CHUNKS)
   uint32_t* claims;     // those counters (claim_index), zeroed one launch ahead by every kernel
+  uint32_t* epoch_dev;  // per local rank r: [r * 16] = the next launch's epoch, [r * 16 + 1] = arrivals
+  int dev_epoch;        // 1: this launch takes its epoch from epoch_dev (CUDA graph mode), else from `epoch`
 };
 
 // Chunk-claim counters: one per (rank, parity set = epoch & 1, slice), 32 bytes

@@ -513,12 +513,12 @@ static_assert(sizeof(ProdState) <= kProdStateBytes, "ProdState must fit its smem
 __device__ __forceinline__ bool flag_seen(const LaneParams& p, const uint32_t* f) {
   uint32_t v;
   asm volatile("ld.relaxed.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-  return (int32_t)(v - p.epoch) >= 0;
+  return (int32_t)(v - cur_epoch()) >= 0;
 }
 __device__ __forceinline__ void fence_acquire_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
 __device__ __forceinline__ bool flag_ready(const LaneParams& p, const uint32_t* f) {
-  return (int32_t)(ld_acquire_sys(f) - p.epoch) >= 0;
+  return (int32_t)(ld_acquire_sys(f) - cur_epoch()) >= 0;
 }
 
 // Blocking acquire-wait on one flag (single thread). false on timeout / abort.
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
       fence_acq_rel_sys();  // release pattern: one fence, then relaxed .sys flag stores
       for (int c = c0; c < c1; ++c) {
         const RelRec& r = rel_rec[c % kRelSlots];
-        for (int i = 0; i < r.n; ++i) st_relaxed_sys(r.f[i], p.epoch);
+        for (int i = 0; i < r.n; ++i) st_relaxed_sys(r.f[i], cur_epoch());
       }
       __threadfence_block();
       for (int c = c0; c < c1; ++c) ring->busy[c % kRelSlots] = 0;
@@ -654,7 +654,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
         atomicExch(cnt, 0u);
         fence_acq_rel_sys();
         for (int q = 0; q < p.P; ++q)
-          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlDone + x.rank, p.epoch);
+          if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlDone + x.rank, cur_epoch());
         for (int q = 0; q < p.P; ++q)
           if (q != x.rank && !wait_one(p, x.me->flags + p.ctl + kCtlDone + q)) break;
         if (tr) p.trace[(size_t)blockIdx.x * kTraceWords + kTrEndAbs] = globaltimer_ns();
@@ -708,7 +708,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
     // on peers' earlier phases of the same chunk, and the lowest unfinished
     // chunk is claimed on every rank.
     const bool dyn = p.dyn != 0;
-    unsigned* const ctr = dyn ? p.claims + claim_index(x.rank, (int)(p.epoch & 1u), l) : nullptr;
+    unsigned* const ctr = dyn ? p.claims + claim_index(x.rank, (int)(cur_epoch() & 1u), l) : nullptr;
     unsigned pending = dyn ? atomicAdd(ctr, 1u) : 0u;
     bool claim_done = !dyn;
     ps->nclaimed = 0;
@@ -737,7 +737,7 @@ __global__ void __launch_bounds__(kThreads, LANE_TMA_MIN_BLOCKS) lane_tma_kernel
         if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlSig + x.rank, my_sig);
       fence_acq_rel_sys();
       for (int q = 0; q < p.P; ++q)
-        if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlEnter + x.rank, p.epoch);
+        if (q != x.rank) st_relaxed_sys(p.rk[q].flags + p.ctl + kCtlEnter + x.rank, cur_epoch());
     }
     // Non-blocking: true once every peer's enter flag is set and the
     // signatures agree (ok = false on a mismatch).

@@ -168,6 +168,7 @@ def main():
             dist.barrier()
             comm.close()
             dist.barrier()
+    failures += graph_cases(P, rank, local)
     ok = torch.tensor([failures])
     dist.all_reduce(ok)
     if rank == 0:
@@ -175,6 +176,74 @@ def main():
               f"in {time.time() - t0:.1f}s", flush=True)
     dist.destroy_process_group()
     sys.exit(1 if ok.item() else 0)
+
+
+def graph_cases(P, rank, local):
+    """CUDA graphs: every rank captures the same three calls (simple on
+    registered buffers, LL, LL128) into a graph and replays it three times
+    with fresh inputs (device-side epochs, lane_kernels.cuh launch_prologue),
+    with an eager call between replays; bit-exact vs the oracle."""
+    failures = 0
+    for (N, G) in layouts(P):
+        os.environ.pop("LANE_PROTO", None)
+        os.environ.pop("LANE_PHASE2", None)
+        os.environ.pop("LANE_DYN_CHUNKS", None)
+        os.environ["LANE_LL128_THRESHOLD_BYTES"] = str(2 << 20)  # 4 MiB: simple protocol
+        os.environ["LANE_LL_THRESHOLD_BYTES"] = str(64 << 10)
+        os.environ["LANE_LL128_MIN_BYTES"] = str(512 << 10)  # 1 MiB: LL128 at every P
+        comm = lane.LaneComm(N, G, 1, rank=rank, device=local)
+        sizes = [(1 << 20) + 5, 3000, (1 << 18) + 3]
+        rin = torch.empty(4 * sizes[0], dtype=torch.uint8, device="cuda")
+        rout = torch.empty_like(rin)
+        comm.register(rin)
+        comm.register(rout)
+        ins = [rin[:4 * sizes[0]].view(torch.float32)] + [torch.empty(n, device="cuda") for n in sizes[1:]]
+        outs = [rout[:4 * sizes[0]].view(torch.float32)] + [torch.empty(n, device="cuda") for n in sizes[1:]]
+        protos = [comm.protocol(n, "float32") for n in sizes]
+        assert protos == ["simple", "ll", "ll128"], protos
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            for i_, o_ in zip(ins, outs):
+                comm.allreduce(o_, i_)
+            g.capture_end()
+        torch.cuda.current_stream().wait_stream(s)
+        for rep in range(3):
+            seed = 3100 + rep
+            for t, n in zip(ins, sizes):
+                sdev.fill(t, "float32", "signed", seed + n, rank)
+            torch.cuda.synchronize()
+            dist.barrier()
+            g.replay()
+            torch.cuda.synchronize()
+            comm.check()
+            for o, n, pr in zip(outs, sizes, protos):
+                xs = [si.generate("float32", "signed", seed + n, p_, n) for p_ in range(P)]
+                ref = oracle.lane_allreduce(xs, N, G, 1, "float32").out[0]
+                if not np.array_equal(bits(to_numpy(o, "float32")), bits(ref)):
+                    print(f"rank {rank} FAIL graph {N}x{G} replay {rep} n={n} proto={pr}", flush=True)
+                    failures += 1
+            n = 4099 + rep  # an eager call between replays
+            inp = sdev.fill(torch.empty(n, device="cuda"), "float32", "signed", 77 + rep, rank)
+            out = torch.empty_like(inp)
+            comm.allreduce(out, inp)
+            torch.cuda.synchronize()
+            comm.check()
+            xs = [si.generate("float32", "signed", 77 + rep, p_, n) for p_ in range(P)]
+            ref = oracle.lane_allreduce(xs, N, G, 1, "float32").out[0]
+            if not np.array_equal(bits(to_numpy(out, "float32")), bits(ref)):
+                print(f"rank {rank} FAIL graph-mode eager {N}x{G} rep {rep}", flush=True)
+                failures += 1
+        os.environ.pop("LANE_LL128_THRESHOLD_BYTES")
+        os.environ.pop("LANE_LL_THRESHOLD_BYTES")
+        os.environ.pop("LANE_LL128_MIN_BYTES")
+        dist.barrier()
+        del g
+        comm.close()
+        dist.barrier()
+    return failures
 
 
 if __name__ == "__main__":

@@ -269,31 +269,71 @@ def test_dynamic_claims_multi_round_few_ctas(mode, monkeypatch):
             assert_parity(got, xs, N, G, "float32", f"claims {mode} ctas={ctas} {N}x{G} k={k}")
 
 
-@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")  # nothing was captured: the call was refused
-def test_graph_capture_is_refused():
-    """A call on a stream being captured into a CUDA graph returns
-    LANE_ERR_UNSUPPORTED (its epoch would be baked into the graph and a replay
-    would read stale data) without launching anything, and the comm stays
-    usable: the next ordinary call is bit-exact."""
+@pytest.mark.filterwarnings("ignore:The CUDA Graph is empty")  # the refused host-API capture records nothing
+def test_cuda_graph_capture_and_replay(monkeypatch):
+    """Calls captured into a CUDA graph (simple, LL and LL128 protocols in one
+    graph) replay correctly: every replay takes a fresh epoch from device
+    memory. Inputs are refilled between replays, eager calls are interleaved
+    with the replays, and every output is bit-exact vs the oracle; the
+    host-buffer API refuses capture with LANE_ERR_UNSUPPORTED."""
     import torch
     import paper_2508_13397_b200 as lane
-    N, G, k, n = 2, 4, 1, 4099
-    e = emu(N, G, k)
-    xs = si.generate_all("float32", "signed", 61, N * G, n)
-    ins = [to_device(x, "float32", "cuda:0") for x in xs]
-    outs = [torch.zeros_like(t) for t in ins]
-    s = torch.cuda.Stream()
-    g = torch.cuda.CUDAGraph()
-    torch.cuda.synchronize()
-    with torch.cuda.stream(s):
-        g.capture_begin()
-        try:
-            with pytest.raises(lane.LaneError) as ei:
-                e.allreduce(outs, ins)
-        finally:
+    from seeded_inputs import device as sdev
+    monkeypatch.setenv("LANE_ROUND_BYTES", str(1 << 30))
+    monkeypatch.setenv("LANE_LL128_THRESHOLD_BYTES", str(2 << 20))  # 4 MiB takes the simple protocol
+    monkeypatch.setenv("LANE_LL_THRESHOLD_BYTES", str(64 << 10))
+    N, G, k = 2, 4, 2
+    P = N * G
+    e = lane.LaneEmulator(N, G, k, device=0)  # fresh: graph mode is sticky per comm
+    try:
+        sizes = [(1 << 20) + 5, 3000, (1 << 18) + 3]  # simple (4 MiB), LL, LL128 (1 MiB)
+        protos = [e.protocol(n, "float32") for n in sizes]
+        assert protos == ["simple", "ll", "ll128"], protos
+        ins = [[torch.empty(n, dtype=torch.float32, device="cuda:0") for _ in range(P)] for n in sizes]
+        outs = [[torch.empty_like(t) for t in row] for row in ins]
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            g.capture_begin()
+            for i_, o_ in zip(ins, outs):
+                e.allreduce(o_, i_)
             g.capture_end()
-    assert ei.value.code == -2 and "capture" in str(ei.value)
-    assert_parity(run(N, G, k, "float32", xs), xs, N, G, "float32", "after a refused capture")
+        torch.cuda.current_stream().wait_stream(s)
+        for rep in range(4):
+            seed = 700 + rep
+            for row in ins:
+                for p, t in enumerate(row):
+                    sdev.fill(t, "float32", "signed", seed, p)
+            torch.cuda.synchronize()
+            g.replay()
+            torch.cuda.synchronize()
+            e.check()
+            for n, row in zip(sizes, outs):
+                xs = si.generate_all("float32", "signed", seed, P, n)
+                assert_parity([to_numpy(o, "float32") for o in row], xs, N, G, "float32", f"replay {rep} n={n}")
+            # an eager call between replays (its epoch also comes from device memory now)
+            n = 4099 + rep
+            xs = si.generate_all("float32", "signed", 900 + rep, P, n)
+            ein = [to_device(x, "float32", "cuda:0") for x in xs]
+            eout = [torch.zeros_like(t) for t in ein]
+            e.allreduce(eout, ein)
+            torch.cuda.synchronize()
+            assert_parity([to_numpy(o, "float32") for o in eout], xs, N, G, "float32", f"eager after replay {rep}")
+        # the host-buffer API cannot be captured
+        hin = [torch.zeros(1024, dtype=torch.float32).pin_memory() for _ in range(P)]
+        hout = [torch.zeros_like(t).pin_memory() for t in hin]
+        g2 = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            g2.capture_begin()
+            try:
+                with pytest.raises(lane.LaneError) as ei:
+                    e.allreduce_host(hout, hin, stream=s)
+            finally:
+                g2.capture_end()
+        assert ei.value.code == -2 and "capture" in str(ei.value)
+    finally:
+        e.close()
 
 
 def test_p1_copy_and_zero_count():
