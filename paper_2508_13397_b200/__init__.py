@@ -26,12 +26,19 @@ def _torch():
     return torch
 
 
+_DTYPE_MAP = None
+
+
 def _dtype_code(t) -> int:
-    torch = _torch()
-    m = {torch.int32: DTYPE["int32"], torch.float32: DTYPE["float32"], torch.bfloat16: DTYPE["bfloat16"]}
-    if t.dtype not in m:
+    global _DTYPE_MAP
+    if _DTYPE_MAP is None:  # built once: the per-call path stays a dict lookup
+        torch = _torch()
+        _DTYPE_MAP = {torch.int32: DTYPE["int32"], torch.float32: DTYPE["float32"],
+                      torch.bfloat16: DTYPE["bfloat16"]}
+    code = _DTYPE_MAP.get(t.dtype)
+    if code is None:
         raise LaneError(-2, f"dtype: {t.dtype} is not supported (int32, float32, bfloat16)")
-    return m[t.dtype]
+    return code
 
 
 def _check_dev_tensor(t, device_index: int, what: str):
@@ -63,10 +70,18 @@ def _check_pair(out, inp, op: str, host: bool = False, device_index: int = 0):
         raise LaneError(-1, "out: must match inp in numel and dtype")
 
 
-def _stream_handle(stream) -> int:
+def _stream_handle(stream, device_index=None) -> int:
+    """Raw cudaStream_t of ``stream`` (default: the current stream of
+    ``device_index``, read without building a torch.cuda.Stream object —
+    the per-call host cost matters for small messages)."""
     torch = _torch()
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    if device_index is not None:
+        raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+        if raw is not None:
+            return int(raw(device_index))
+    return int(torch.cuda.current_stream().cuda_stream)
 
 
 def version() -> str:
@@ -196,7 +211,7 @@ class LaneComm(_CommBase):
         current). ``out is inp`` (same storage) is in-place."""
         _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
-                                          _dtype_code(inp), 0, _stream_handle(stream))
+                                          _dtype_code(inp), 0, _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return out
 
@@ -206,7 +221,7 @@ class LaneComm(_CommBase):
         reduction order with per-hop rounding."""
         _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce_ring(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
-                                               _dtype_code(inp), 0, _stream_handle(stream))
+                                               _dtype_code(inp), 0, _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return out
 
@@ -215,7 +230,7 @@ class LaneComm(_CommBase):
         of the whole buffer): same results as ``allreduce``, more traffic."""
         _check_pair(out, inp, op, device_index=self.device)
         code = _lib.load().lane_allreduce_approach2(self._comm, inp.data_ptr(), out.data_ptr(), inp.numel(),
-                                                    _dtype_code(inp), 0, _stream_handle(stream))
+                                                    _dtype_code(inp), 0, _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return out
 
@@ -303,28 +318,28 @@ class LaneEmulator(_CommBase):
 
     def allreduce(self, outs, inps, op: str = "sum", stream=None):
         code = _lib.load().lane_allreduce_emulated(self._comm, *self._args(outs, inps, op), 0,
-                                                   _stream_handle(stream))
+                                                   _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return outs
 
     def allreduce_ring(self, outs, inps, op: str = "sum", stream=None):
         """Ring allreduce (Alg. 1) of all emulated ranks."""
         code = _lib.load().lane_allreduce_ring_emulated(self._comm, *self._args(outs, inps, op), 0,
-                                                        _stream_handle(stream))
+                                                        _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return outs
 
     def allreduce_approach2(self, outs, inps, op: str = "sum", stream=None):
         """'Approach 2' (node allreduce, then lane allreduce) of all emulated ranks."""
         code = _lib.load().lane_allreduce_approach2_emulated(self._comm, *self._args(outs, inps, op), 0,
-                                                             _stream_handle(stream))
+                                                             _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         return outs
 
     def allreduce_host(self, outs_host, inps_host, op: str = "sum", stream=None):
         torch = _torch()
         code = _lib.load().lane_allreduce_emulated_host(self._comm, *self._args(outs_host, inps_host, op, dev=False),
-                                                        0, _stream_handle(stream))
+                                                        0, _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
         (stream or torch.cuda.current_stream()).synchronize()
         return outs_host
