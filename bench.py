@@ -859,20 +859,31 @@ class NcclPPG:
     GPU, each running a standard NCCL allreduce on its own 1/PPG slice of the
     buffer on its own stream (P L269 §2.2, P L504 §4.2)."""
 
-    def __init__(self, ppg, dist):
+    def __init__(self, ppg, dist, backend="nccl"):
         import torch
         self.ppg = ppg
-        self.groups = [dist.new_group(backend="nccl") for _ in range(ppg)]
-        self.streams = [torch.cuda.Stream() for _ in range(ppg)]
+        self.groups = [dist.new_group(backend=backend) for _ in range(ppg)]
+        self.streams = [torch.cuda.Stream() for _ in range(ppg)] if backend == "nccl" else None
+
+    @staticmethod
+    def slices(n, ppg, q=4):
+        """[a, b) of every communicator's slice: contiguous, covering [0, n),
+        boundaries on q elements (16 B for fp32/int32)."""
+        out = []
+        for i in range(ppg):
+            a = (n * i // ppg) // q * q
+            b = n if i == ppg - 1 else (n * (i + 1) // ppg) // q * q
+            out.append((a, b))
+        return out
 
     def run(self, buf, dist):
         import torch
+        if self.streams is None:  # CPU (gloo) test of the slicing: one communicator after the other
+            for (a, b), g in zip(self.slices(buf.numel(), self.ppg), self.groups):
+                dist.all_reduce(buf[a:b], group=g)
+            return
         cur = torch.cuda.current_stream()
-        n = buf.numel()
-        q = 4  # slice boundaries on 16 B for fp32/int32 (8 for bf16 is also fine)
-        for i, (g, st) in enumerate(zip(self.groups, self.streams)):
-            a = (n * i // self.ppg) // q * q
-            b = n if i == self.ppg - 1 else (n * (i + 1) // self.ppg) // q * q
+        for (a, b), g, st in zip(self.slices(buf.numel(), self.ppg), self.groups, self.streams):
             st.wait_stream(cur)
             with torch.cuda.stream(st):
                 dist.all_reduce(buf[a:b], group=g)

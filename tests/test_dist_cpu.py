@@ -86,7 +86,36 @@ def _max_over_ranks(rank, world):
     return bench.max_over_ranks(1.5 + 2.25 * rank)
 
 
+def _nccl_ppg_slices(rank, world):
+    import torch
+    import bench
+    ppg = bench.NcclPPG(4, dist, backend="gloo")
+    res = {}
+    for n in (1, 7, 64, 4099, 100003):
+        buf = torch.arange(n, dtype=torch.float32) * (rank + 1)
+        ppg.run(buf, dist)
+        want = torch.arange(n, dtype=torch.float32) * sum(r + 1 for r in range(world))
+        res[n] = bool(torch.equal(buf, want))
+    return res
+
+
 # ----------------------------------------------------------------- tests
+def test_nccl_ppg_comparator_slices():
+    """The multi-PPG CCL comparator (P L269, L504): PPG
+    communicators each allreduce one slice; the slices are contiguous, cover
+    the buffer exactly with 16-byte boundaries, and together give the full
+    allreduce (gloo stand-in for NCCL, world size 2)."""
+    import bench
+    for n in (0, 1, 7, 64, 4099, 1 << 20):
+        for ppg in (1, 2, 4, 16):
+            sl = bench.NcclPPG.slices(n, ppg)
+            assert sl[0][0] == 0 and sl[-1][1] == n
+            assert all(b0 == a1 for (_, b0), (a1, _) in zip(sl, sl[1:]))
+            assert all(a % 4 == 0 for a, _ in sl)
+    out = _spawn("_nccl_ppg_slices")
+    assert all(all(v.values()) for v in out.values()), out
+
+
 def test_exchange_blobs_rank_order_gloo():
     out = _spawn("_exchange")
     want = [(bytes([r + 1]) * 64 + r.to_bytes(4, "little")).hex() for r in range(2)]
