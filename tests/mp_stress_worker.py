@@ -75,7 +75,8 @@ def main():
     ap.add_argument("--layouts", default="default", help="'all', 'default' (2 x P/2) or NxG")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    local = int(os.environ.get("LOCAL_RANK", rank))
+    # LANE_TEST_DEVICE=d puts every rank on GPU d (ranks sharing one GPU: the 1-GPU tier)
+    local = int(os.environ.get("LANE_TEST_DEVICE", os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     os.environ.setdefault("LANE_TIMEOUT_MS", "10000")

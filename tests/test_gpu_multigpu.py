@@ -62,3 +62,54 @@ def test_stress_back_to_back(P):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "mp_stress_worker" in out and ": OK" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_ranks_sharing_one_gpu(P):
+    """P processes on cuda:0 through the multi-GPU code path (same-device IPC
+    peers, system-scope flags, the start handshake and end barrier, staged and
+    registered buffers, every layout of P, k = 1 and 2, simple / bulk stores /
+    chunk claims / LL / LL128, fp32 / bf16 / int32) bit-exactly against the
+    oracle — so a box with ONE GPU runs the IPC path too (their kernels share
+    the GPU; every cross-rank wait is bounded by the watchdog). P = 2 about
+    10 s, P = 4 about 60 s on a B200 (profiles/r02_samedev.txt)."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29640 + P),
+           os.path.join(ROOT, "tests", "mp_samedev_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_samedev_worker: OK" in out, out[-4000:]
+
+
+def test_watchdog_and_mismatch_sharing_one_gpu():
+    """test_watchdog_timeout_p2's cases (watchdog on a call a peer never joins;
+    LANE_ERR_MISMATCH from the start handshake) with both ranks on cuda:0."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", "29651",
+           os.path.join(ROOT, "tests", "mp_timeout_worker.py")]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, cwd=ROOT,
+                       env=dict(os.environ, LANE_TEST_DEVICE="0"))
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_timeout_worker: OK" in out, out[-4000:]
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_stress_sharing_one_gpu(P):
+    """test_stress_back_to_back (every layout of P, every protocol threshold,
+    bit-exact per call) with all P ranks on cuda:0, 300 calls per layout."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29660 + P),
+           os.path.join(ROOT, "tests", "mp_stress_worker.py"), "--iters", "300", "--layouts", "all"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
+                       env=dict(os.environ, LANE_TEST_DEVICE="0"))
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_stress_worker" in out and ": OK" in out, out[-4000:]
