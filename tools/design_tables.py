@@ -55,6 +55,29 @@ def sweep_table(paths):
     return "\n".join(out)
 
 
+def std_table(paths):
+    """The paper's standard-vs-lane comparison (fig:std_vs_lane, P L401, L457)
+    from sweep rows that carry the Alg. 1 ring and approach 2 columns."""
+    out = []
+    for path in paths:
+        rs = [r for r in rows(path) if r.get("verified") and "lane_ring_alg1_busbw" in r]
+        bad = [r for r in rs if not clocks_ok(r)]
+        out.append(f"`{path}` (busbw GB/s, median of {rs[0].get('repeats', 1)}; lane and approach 2 whole-buffer "
+                   f"verified bit-exactly, ring on its first 2^16 elements within the per-hop bound; {len(bad)} rows without a clean clock record)\n")
+        out.append("| layout | MiB per rank | lane method | Alg. 1 ring (ours) | lane / ring | approach 2 | NCCL ring |")
+        out.append("|---|---|---|---|---|---|---|")
+        for r in rs:
+            out.append(f"| {r['layout']} | {r['bytes'] >> 20} | {r['busbw']:.0f}{LETTER.get(r['protocol'], '')} | "
+                       f"{r['lane_ring_alg1_busbw']:.0f}{LETTER.get(r.get('ring_protocol'), '')} | "
+                       f"{r['busbw'] / r['lane_ring_alg1_busbw']:.2f}× | "
+                       f"{r['approach2_busbw']:.0f} | {r.get('nccl_ring_busbw', float('nan')):.0f} |"
+                       if "approach2_busbw" in r else
+                       f"| {r['layout']} | {r['bytes'] >> 20} | {r['busbw']:.0f} | {r['lane_ring_alg1_busbw']:.0f} | "
+                       f"{r['busbw'] / r['lane_ring_alg1_busbw']:.2f}× | — | {r.get('nccl_ring_busbw', float('nan')):.0f} |")
+        out.append("")
+    return "\n".join(out)
+
+
 def matrix_table(paths):
     out = []
     for path in paths:
@@ -82,11 +105,14 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("sweeps", nargs="*")
     ap.add_argument("--matrix", nargs="*", default=[])
+    ap.add_argument("--std", nargs="*", default=[], help="sweeps with --ring --approach2 columns")
     a = ap.parse_args()
     if a.sweeps:
         print(sweep_table(a.sweeps))
     if a.matrix:
         print(matrix_table(a.matrix))
+    if a.std:
+        print(std_table(a.std))
 
 
 if __name__ == "__main__":
