@@ -3,7 +3,9 @@ code path — IPC-mapped peer memory (same-device IPC handles), system-scope
 epoch flags, the start handshake with the call signature and the end barrier,
 registered (zero-copy) and staged buffers — on a box with a single GPU, where
 the kernels of the P processes share the GPU (every cross-rank wait is
-bounded by the watchdog). Every layout N x G of P, k = 1 and 2, simple /
+bounded by the watchdog). LANE_TEST_GPUS=g spreads the ranks over g GPUs
+(rank % g), so P = 8 runs on a 1- or 2-GPU box, some peers local and some over
+NVLink. Every layout N x G of P, k = 1 and 2, simple /
 bulk stores / chunk claims / LL / LL128, fp32 / bf16 / int32, 5 to 2^20 + 3
 elements.
 
@@ -31,20 +33,24 @@ from tests.gpu_util import bits, to_numpy  # noqa: E402
 
 def main():
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    torch.cuda.set_device(0)
+    dev = rank % int(os.environ.get("LANE_TEST_GPUS", "1"))  # > 1: some peers local, some over NVLink
+    torch.cuda.set_device(dev)
     dist.init_process_group("gloo")
     os.environ.setdefault("LANE_TIMEOUT_MS", "60000")
     t0 = time.time()
     failures = 0
     layouts = [(N, world // N) for N in range(1, world + 1) if world % N == 0]
-    cases = [(N, G, k, proto) for (N, G) in layouts for k in (1, 2)
-             for proto in ("simple", "simple-bulk", "simple-claims", "ll", "ll128")]
+    protos = ("simple", "simple-bulk", "simple-claims", "ll", "ll128")
+    ks = (1, 2)
+    if "--quick" in sys.argv:  # P = 8 on one or two GPUs: every layout and protocol, fewer k
+        ks = (1,)
+    cases = [(N, G, k, proto) for (N, G) in layouts for k in ks for proto in protos]
     tdts = {"int32": torch.int32, "float32": torch.float32, "bfloat16": torch.bfloat16}
     for N, G, k, proto in cases:
         os.environ["LANE_PROTO"] = proto.split("-")[0]
         os.environ["LANE_STORE"] = "bulk" if proto == "simple-bulk" else "auto"
         os.environ["LANE_DYN_CHUNKS"] = "1" if proto == "simple-claims" else "-1"
-        comm = lane.LaneComm(N, G, k, rank=rank, device=0)
+        comm = lane.LaneComm(N, G, k, rank=rank, device=dev)
         n_max = (1 << 20) + 3
         rin = torch.empty(4 * n_max, dtype=torch.uint8, device="cuda")
         rout = torch.empty_like(rin)

@@ -75,8 +75,12 @@ def main():
     ap.add_argument("--layouts", default="default", help="'all', 'default' (2 x P/2) or NxG")
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
-    # LANE_TEST_DEVICE=d puts every rank on GPU d (ranks sharing one GPU: the 1-GPU tier)
-    local = int(os.environ.get("LANE_TEST_DEVICE", os.environ.get("LOCAL_RANK", rank)))
+    # LANE_TEST_DEVICE=d puts every rank on GPU d (ranks sharing one GPU: the 1-GPU tier);
+    # LANE_TEST_GPUS=g spreads the ranks over g GPUs (rank % g; P = 8 on fewer GPUs)
+    if "LANE_TEST_GPUS" in os.environ:
+        local = rank % int(os.environ["LANE_TEST_GPUS"])
+    else:
+        local = int(os.environ.get("LANE_TEST_DEVICE", os.environ.get("LOCAL_RANK", rank)))
     torch.cuda.set_device(local)
     dist.init_process_group("gloo")
     os.environ.setdefault("LANE_TIMEOUT_MS", "10000")

@@ -113,3 +113,38 @@ def test_stress_sharing_one_gpu(P):
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert "mp_stress_worker" in out and ": OK" in out, out[-4000:]
+
+
+def _p8_env():
+    return dict(os.environ, LANE_TEST_GPUS=str(1 if _ngpus() < 2 else 2))
+
+
+def test_p8_ranks_sharing_gpus():
+    """P = 8 through the multi-process path on a 1- or 2-GPU box (8 ranks on one
+    GPU, or 4 + 4 with peers both local and over NVLink): every P = 8 layout
+    (1x8, 2x4, 4x2, 8x1), simple / bulk stores / chunk claims / LL / LL128,
+    fp32 / bf16 / int32, bit-exact vs the oracle. About 90 s on one B200
+    (profiles/r02_p8_shared.txt)."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", "29671",
+           os.path.join(ROOT, "tests", "mp_samedev_worker.py"), "--quick"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=_p8_env())
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "mp_samedev_worker: OK" in out, out[-4000:]
+
+
+def test_p8_stress_sharing_gpus():
+    """The exact stress at P = 8 (every layout, 300 calls each, up to 7 writers
+    per destination) with the 8 ranks on one or two GPUs."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", "29672",
+           os.path.join(ROOT, "tests", "mp_stress_worker.py"), "--iters", "300", "--layouts", "all"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT, env=_p8_env())
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert out.count(": OK (0 bad calls") == 4, out[-4000:]
