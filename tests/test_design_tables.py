@@ -32,3 +32,36 @@ def test_design_table_rendered_from_profile(args):
         design = f.read()
     missing = [ln for ln in rows if ln not in design]
     assert not missing, missing[:3]
+
+
+def _bench_rows():
+    with open(os.path.join(ROOT, "DESIGN.md")) as f:
+        for ln in f:
+            if ln.startswith("| ") and "_final.jsonl` |" in ln and "bench_n" in ln:
+                yield ln
+
+
+def test_bench_line_table_matches_files():
+    """DESIGN §8's bench-line table (hand-written) agrees with the JSON lines it
+    cites: value, ms per call, NCCL ring / ×4 PPG / default, staged, e2e and the
+    roofline fraction, to the digits shown."""
+    import json
+    import re
+    rows = list(_bench_rows())
+    assert len(rows) >= 3
+    for ln in rows:
+        cells = [c.strip() for c in ln.strip().strip("|").split("|")]
+        path = re.search(r"`([^`]+\.jsonl)`", cells[-1]).group(1)
+        with open(os.path.join(ROOT, "profiles", path)) as f:
+            d = json.loads(f.readline())
+
+        val = lambda k: (d.get(k) or {}).get("value")  # noqa: E731
+        want = [d["value"], d["ms_per_step"], val("nccl_ring"), val("nccl_ring_multi_ppg"),
+                val("nccl_default_context"), val("staged"), d["e2e"]["value"], d["roofline"]["frac"]]
+        for c, w in zip(cells[2:10], want):
+            s = c.replace("*", "").split()[0]
+            if s == "—":
+                assert w is None, (path, c, w)
+                continue
+            decimals = len(s.split(".")[1]) if "." in s else 0
+            assert w is not None and abs(float(s) - w) <= 0.5 * 10 ** -decimals + 1e-9, (path, c, w)
