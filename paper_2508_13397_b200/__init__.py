@@ -262,9 +262,9 @@ class LaneComm(_CommBase):
         _check_pair(out_host, inp_host, op, host=True)
         code = _lib.load().lane_allreduce_host(self._comm, inp_host.data_ptr(), out_host.data_ptr(),
                                                inp_host.numel(), _dtype_code(inp_host), 0,
-                                               _stream_handle(stream))
+                                               _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
-        (stream or torch.cuda.current_stream()).synchronize()
+        (stream or torch.cuda.current_stream(self.device)).synchronize()
         return out_host
 
 
@@ -341,5 +341,5 @@ class LaneEmulator(_CommBase):
         code = _lib.load().lane_allreduce_emulated_host(self._comm, *self._args(outs_host, inps_host, op, dev=False),
                                                         0, _stream_handle(stream, self.device))
         _lib.check(code, self._comm)
-        (stream or torch.cuda.current_stream()).synchronize()
+        (stream or torch.cuda.current_stream(self.device)).synchronize()
         return outs_host
