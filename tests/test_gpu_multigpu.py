@@ -148,3 +148,23 @@ def test_p8_stress_sharing_gpus():
     out = r.stdout + r.stderr
     assert r.returncode == 0, out[-4000:]
     assert out.count(": OK (0 bad calls") == 4, out[-4000:]
+
+
+def test_p8_baseline_fullsize_sharing_gpus():
+    """BASELINE configs[1] at P = 8 and full size (2x4, fp32, 1 GiB per rank)
+    through the multi-process path with the 8 ranks on one or two GPUs: every
+    output element of every rank bit-exact on the device
+    (tools/p8_fullsize_check.py; profiles/r02_p8_fullsize_shared.txt)."""
+    if _ngpus() < 1:
+        pytest.skip("needs a GPU")
+    import torch
+    free = torch.cuda.mem_get_info(0)[0]
+    if free < (48 << 30):
+        pytest.skip("needs ~48 GiB free on GPU 0")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=8",
+           "--master-addr", "127.0.0.1", "--master-port", "29673",
+           os.path.join(ROOT, "tools", "p8_fullsize_check.py"), "--layouts", "2x4", "--mib", "1024", "--calls", "1"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT, env=_p8_env())
+    out = r.stdout + r.stderr
+    assert r.returncode == 0, out[-4000:]
+    assert "p8_fullsize_check 2x4 k=1 float32 1024 MiB/rank" in out and ": OK (2147483648 elements" in out, out[-4000:]
