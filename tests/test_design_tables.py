@@ -65,3 +65,14 @@ def test_bench_line_table_matches_files():
                 continue
             decimals = len(s.split(".")[1]) if "." in s else 0
             assert w is not None and abs(float(s) - w) <= 0.5 * 10 ** -decimals + 1e-9, (path, c, w)
+
+
+def test_clocks_ok_rejects_throttled_rows():
+    sys.path.insert(0, os.path.join(ROOT, "tools"))
+    import design_tables as dt
+    assert dt.clocks_ok({"clocks": {"samples": 5, "reasons": []}})
+    assert dt.clocks_ok({"clocks": {"samples": 5, "reasons": ["sw_power_cap"]}})  # kept and noted
+    for r in ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"):
+        assert not dt.clocks_ok({"clocks": {"samples": 5, "reasons": [r]}})
+    assert not dt.clocks_ok({"clocks": {"samples": 0, "reasons": []}})
+    assert not dt.clocks_ok({})
