@@ -41,3 +41,18 @@ def test_cited_profiles_exist(doc):
             if not any(glob.glob(c) for c in cands):
                 missing.append(name)
     assert not missing, missing
+
+
+@pytest.mark.parametrize("doc", DOCS)
+def test_cited_source_paths_exist(doc):
+    with open(os.path.join(ROOT, doc)) as f:
+        text = f.read()
+    missing = []
+    for tok in re.findall(r"`([^`]+)`", text):
+        for word in tok.split():
+            word = word.strip(",;:()")
+            if re.match(r"(tools|tests|include|oracle|seeded_inputs|paper_2508_13397_b200)/[\w./{},*-]+$", word):
+                for name in expand(word.split(":")[0]):
+                    if not glob.glob(os.path.join(ROOT, name)):
+                        missing.append(name)
+    assert not missing, missing
