@@ -5,7 +5,6 @@ plain torch kernel launch, median wall time per call over many calls
 
 torchrun --nproc-per-node 2 tools/host_overhead.py
 """
-import ctypes
 import os
 import statistics
 import sys
